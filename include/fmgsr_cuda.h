@@ -1,0 +1,171 @@
+/*
+ * fmgsr_cuda.h -- C ABI of libfmgsr_cuda.so, the B200 (sm_100a) hot path of
+ * the FMG-FAS solver with segmental refinement (arXiv 1207.6720, 1D model
+ * problem).  This is the drop-in boundary for the reference's kernel-lane
+ * interface; citations are into the reference package
+ * (/root/reference/pkg/src/fmgsr/).
+ *
+ * Conventions
+ *   - Every field pointer is a DEVICE pointer to a row-major [n][ld] array:
+ *     cell index major, right-hand side (RHS) fastest, B <= ld active RHS
+ *     columns.  B = 1, ld = 1 is the reference's single 1-D float64 field.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     asynchronous and stream-ordered; no call synchronises the device.
+ *   - The library never allocates on the per-call path (the plan allocates
+ *     its level workspace once, at fmgsr_plan_create).
+ *   - Return 0 on success, a negative code on failure (-1 bad argument,
+ *     -2 CUDA error, -3 internal); fmgsr_last_error() has the message (per
+ *     host thread).  The Python layer re-raises these as ValueError /
+ *     RuntimeError, mirroring the reference's argument checks.
+ *   - _f64 computes in IEEE binary64 with the reference's exact operation
+ *     order and no FMA contraction (bit-identical to the numba lane);
+ *     _f32 is the same algorithm in binary32.
+ */
+#ifndef FMGSR_CUDA_H
+#define FMGSR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMGSR_ABI_VERSION 1
+
+int fmgsr_abi_version(void);
+const char* fmgsr_last_error(void);
+
+/* ---- Kernel-lane entry points (reference _kernels_numba.py) ------------- */
+
+/* replaces gs_sweep(u, f, inv_h2, start, stop, forward, omega),
+ * _kernels_numba.py:15-36 / _kernels_numpy.py:13-35; in place on u. */
+int fmgsr_gs_sweep_f64(double* u, const double* f, int64_t n, int64_t B, int64_t ld,
+                       double inv_h2, int64_t start, int64_t stop, int forward, double omega,
+                       void* stream);
+int fmgsr_gs_sweep_f32(float* u, const float* f, int64_t n, int64_t B, int64_t ld, double inv_h2,
+                       int64_t start, int64_t stop, int forward, double omega, void* stream);
+
+/* replaces kaczmarz_sweep(u, u_coarse, start, stop, forward, proj_diag),
+ * _kernels_numba.py:39-57; in place on u; uc is [n/2][ld].  Pairs are
+ * disjoint, so `forward` does not change the result (kept for the ABI). */
+int fmgsr_kaczmarz_sweep_f64(double* u, const double* uc, int64_t n, int64_t B, int64_t ld,
+                             int64_t start, int64_t stop, int forward, double proj_diag,
+                             void* stream);
+int fmgsr_kaczmarz_sweep_f32(float* u, const float* uc, int64_t n, int64_t B, int64_t ld,
+                             int64_t start, int64_t stop, int forward, double proj_diag,
+                             void* stream);
+
+/* replaces smooth_patches(u_in, f, inv_h2, owned_lo, owned_hi, ext_lo, ext_hi,
+ * ns, omega, use_cr, u_coarse, proj_diag) -> u_out, _kernels_numba.py:60-92.
+ * Patch arrays are DEVICE int64[P].  u_out must not alias u_in (the
+ * reference returns a new array).  inv_h2 must equal 4^log2(n).
+ * ns >= 2 needs a scratch of fmgsr_smooth_scratch_rows() rows x
+ * round_up(B, 32) elements (row stride sld), and scratch_off (device
+ * int64[P]) = exclusive prefix sum of the per-patch rows
+ * (min(n, ext_hi + 1) - max(0, ext_lo - 1)); both may be NULL when ns == 1. */
+int fmgsr_smooth_patches_f64(const double* u_in, const double* f, double* u_out, int64_t n,
+                             int64_t B, int64_t ld, double inv_h2, const int64_t* owned_lo,
+                             const int64_t* owned_hi, const int64_t* ext_lo,
+                             const int64_t* ext_hi, int64_t P, int64_t ns, double omega,
+                             int use_cr, const double* uc, double proj_diag, double* scratch,
+                             const int64_t* scratch_off, int64_t sld, void* stream);
+int fmgsr_smooth_patches_f32(const float* u_in, const float* f, float* u_out, int64_t n,
+                             int64_t B, int64_t ld, double inv_h2, const int64_t* owned_lo,
+                             const int64_t* owned_hi, const int64_t* ext_lo,
+                             const int64_t* ext_hi, int64_t P, int64_t ns, double omega,
+                             int use_cr, const float* uc, double proj_diag, float* scratch,
+                             const int64_t* scratch_off, int64_t sld, void* stream);
+
+/* Uniform patch geometry (owned width W | n, b-cell buffer, clamped): the
+ * reference partition() (mesh.py:102-136) is W = 2, b = halo; global mode is
+ * W = n, b = 0; the generalised P-patch geometry is W = max(2, n/P). */
+int64_t fmgsr_smooth_scratch_rows(int64_t n, int64_t W, int64_t b);
+int fmgsr_smooth_uniform_f64(const double* u_in, const double* f, double* u_out, int64_t n,
+                             int64_t B, int64_t ld, int64_t W, int64_t b, int64_t ns,
+                             double omega, const double* uc, double proj_diag, double* scratch,
+                             int64_t sld, void* stream);
+int fmgsr_smooth_uniform_f32(const float* u_in, const float* f, float* u_out, int64_t n,
+                             int64_t B, int64_t ld, int64_t W, int64_t b, int64_t ns,
+                             double omega, const float* uc, double proj_diag, float* scratch,
+                             int64_t sld, void* stream);
+
+/* ---- Level operators (reference stencils.py, smoothers.py) -------------- */
+/* apply_operator, stencils.py:27-36: out[n] = L_k u */
+int fmgsr_apply_operator_f64(const double* u, double* out, int64_t n, int64_t B, int64_t ld, void* stream);
+int fmgsr_apply_operator_f32(const float* u, float* out, int64_t n, int64_t B, int64_t ld, void* stream);
+/* restrict, stencils.py:39-47: out[n_fine/2] */
+int fmgsr_restrict_f64(const double* u, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_restrict_f32(const float* u, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+/* prolong_correction, stencils.py:50-64: out[2 n_coarse] */
+int fmgsr_prolong_correction_f64(const double* c, double* out, int64_t n_coarse, int64_t B, int64_t ld, void* stream);
+int fmgsr_prolong_correction_f32(const float* c, float* out, int64_t n_coarse, int64_t B, int64_t ld, void* stream);
+/* prolong_fmg, stencils.py:67-105: out[2 n_coarse], n_coarse >= 4 */
+int fmgsr_prolong_fmg_f64(const double* c, double* out, int64_t n_coarse, int64_t B, int64_t ld, void* stream);
+int fmgsr_prolong_fmg_f32(const float* c, float* out, int64_t n_coarse, int64_t B, int64_t ld, void* stream);
+/* tau_correction, stencils.py:108-116: out[n_fine/2] */
+int fmgsr_tau_correction_f64(const double* u, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_tau_correction_f32(const float* u, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+/* coarse_rhs, stencils.py:119-125: out = restrict(f) + tau(u) */
+int fmgsr_coarse_rhs_f64(const double* f, const double* u, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_coarse_rhs_f32(const float* f, const float* u, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+/* FAS correction update, cycles.py:120-121: out = u + P(uH - R u) */
+int fmgsr_fas_correct_f64(const double* u, const double* uH, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_fas_correct_f32(const float* u, const float* uH, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+/* direct_solve, smoothers.py:210-225 (LAPACK ?ptsv order), n <= 2048 */
+int fmgsr_direct_solve_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, void* stream);
+int fmgsr_direct_solve_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, void* stream);
+/* same for any n, with a DEVICE workspace of 2n elements for the factor
+ * (also backs problem.direct_fine_solve, problem.py:61-77) */
+int fmgsr_direct_solve_ws_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, double* workspace, void* stream);
+int fmgsr_direct_solve_ws_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* workspace, void* stream);
+
+/* ---- Synthetic inputs (BASELINE.json configs; not on the solve path) ---- */
+/* f = sum_k coef[r][k-1] sin(k pi x), uex = sum_k coef sin(k pi x)/(k pi)^2;
+ * coef is a DEVICE double[B][K]; uex may be NULL. */
+int fmgsr_fourier_rhs_f64(const double* coef, int K, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* stream);
+int fmgsr_fourier_rhs_f32(const double* coef, int K, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* stream);
+/* nonlinear manufactured problem (config 3): u = s x(1-x)e^x, f = -u'' + u^3;
+ * scale is a DEVICE double[B]; uex may be NULL. */
+int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* stream);
+int fmgsr_nonlinear_rhs_f32(const double* scale, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* stream);
+
+/* ---- Whole-solve plan: fmg_solve (cycles.py:137-222) -------------------- */
+typedef struct fmgsr_plan_desc {
+  int32_t m0, m;      /* hierarchy 2^m0 .. 2^m (cycles.py:39-49 limits) */
+  int32_t n_sr;       /* segmental-refinement depth, 0 <= n_sr <= m-m0-1 */
+  int32_t ns;         /* inner sweeps: V(ns,ns) */
+  int32_t geom_mode;  /* 0 = reference halo (W=2,b), 1 = global, 2 = P patches */
+  int32_t dtype;      /* 0 = f64, 1 = f32 */
+  int64_t P;          /* patches on the finest level (geom_mode 2) */
+  int64_t b;          /* buffer / halo cells */
+  int64_t B;          /* right-hand sides per solve */
+  int64_t ld;         /* row stride of forcing / solution (>= B) */
+  double omega;       /* relaxation weight (reference: 1.0) */
+  int32_t fused;      /* 1: fused level visits where eligible; 0: operator-by-operator */
+  int32_t use_graph;  /* 1: capture the cycle in a CUDA graph per (in, out) pair */
+} fmgsr_plan_desc;
+
+typedef struct fmgsr_plan_info {
+  int64_t workspace_bytes;
+  int64_t launches_per_solve;   /* kernels + memsets issued by one solve */
+  int64_t visits_per_solve;     /* level visits (smooths + direct solves) */
+  double alg_bytes_per_solve;   /* compulsory HBM traffic model */
+  double finest_visit_alg_bytes;/* algorithmic bytes of one finest-level visit */
+} fmgsr_plan_info;
+
+int fmgsr_plan_create(const fmgsr_plan_desc* desc, void** plan);
+int fmgsr_plan_destroy(void* plan);
+int fmgsr_plan_get_info(void* plan, fmgsr_plan_info* info);
+/* One FMG-FAS(-SR) solve of B RHS: forcing, solution are DEVICE [2^m][ld]. */
+int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stream);
+/* Same solve launched op by op (no graph) with per-visit CUDA events for
+ * profiling: writes up to `cap` visit durations (ms) and their levels. */
+int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,
+                           float* visit_ms, int32_t* visit_level, int32_t* visit_kind,
+                           int64_t cap, int64_t* n_visits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FMGSR_CUDA_H */

@@ -1,0 +1,156 @@
+"""Loader of ``libfmgsr_cuda.so`` (the sm_100a kernels behind the C ABI of
+``include/fmgsr_cuda.h``).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+entry point raises.  ``lib()`` binds ctypes signatures once; ``call`` turns a
+negative return code into ``ValueError`` (bad argument, mirroring the
+reference's argument checks) or ``RuntimeError`` (CUDA failure).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmgsr_cuda.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+_i64 = C.c_int64
+_i32 = C.c_int32
+_vp = C.c_void_p
+_d = C.c_double
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("m0", _i32), ("m", _i32), ("n_sr", _i32), ("ns", _i32),
+        ("geom_mode", _i32), ("dtype", _i32),
+        ("P", _i64), ("b", _i64), ("B", _i64), ("ld", _i64),
+        ("omega", _d), ("fused", _i32), ("use_graph", _i32),
+    ]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("workspace_bytes", _i64), ("launches_per_solve", _i64),
+        ("visits_per_solve", _i64), ("alg_bytes_per_solve", _d),
+        ("finest_visit_alg_bytes", _d),
+    ]
+
+
+_SIGS = {
+    "fmgsr_abi_version": (C.c_int, []),
+    "fmgsr_last_error": (C.c_char_p, []),
+    "fmgsr_gs_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _d, _i64, _i64, C.c_int, _d, _vp]),
+    "fmgsr_kaczmarz_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _d, _vp]),
+    "fmgsr_smooth_patches": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _vp, _vp, _vp, _vp,
+                                       _i64, _i64, _d, C.c_int, _vp, _d, _vp, _vp, _i64, _vp]),
+    "fmgsr_smooth_uniform": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _d,
+                                       _vp, _d, _vp, _i64, _vp]),
+    "fmgsr_apply_operator": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_restrict": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_prolong_correction": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_prolong_fmg": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_tau_correction": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_coarse_rhs": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_fas_correct": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_direct_solve": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_direct_solve_ws": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "fmgsr_fourier_rhs": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "fmgsr_nonlinear_rhs": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "fmgsr_smooth_scratch_rows": (_i64, [_i64, _i64, _i64]),
+    "fmgsr_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_vp)]),
+    "fmgsr_plan_destroy": (C.c_int, [_vp]),
+    "fmgsr_plan_get_info": (C.c_int, [_vp, C.POINTER(PlanInfo)]),
+    "fmgsr_plan_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "fmgsr_plan_solve_timed": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                                         C.POINTER(_i64)]),
+}
+_TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmgsr_smooth_uniform",
+          "fmgsr_apply_operator", "fmgsr_restrict", "fmgsr_prolong_correction",
+          "fmgsr_prolong_fmg", "fmgsr_tau_correction", "fmgsr_coarse_rhs", "fmgsr_fas_correct",
+          "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_fourier_rhs",
+          "fmgsr_nonlinear_rhs"}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def build(force: bool = False) -> str:
+    """Compile the extension in-tree with nvcc for sm_100a (csrc/Makefile)."""
+    args = ["make", "-s", "-C", CSRC]
+    if force:
+        subprocess.run(args + ["clean"], check=True)
+    subprocess.run(args, check=True)
+    return LIB_PATH
+
+
+def exported_symbols() -> list[str]:
+    """Every C symbol the header declares (for the ABI export test)."""
+    out = []
+    for name in _SIGS:
+        if name in _TYPED:
+            out += [name + "_f64", name + "_f32"]
+        else:
+            out.append(name)
+    return out
+
+
+def lib():
+    """The loaded library with bound signatures (raises if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libfmgsr_cuda.so not found at {LIB_PATH}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        h = C.CDLL(LIB_PATH)
+        for name in exported_symbols():
+            base = name[:-4] if name.endswith(("_f64", "_f32")) and name[:-4] in _TYPED else name
+            restype, argtypes = _SIGS[base]
+            fn = getattr(h, name)
+            fn.restype = restype
+            fn.argtypes = argtypes
+        _lib = h
+    return _lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("fmgsr_b200 needs a CUDA device (B200, sm_100a); there is no CPU path")
+
+
+def fn(name: str, dtype: torch.dtype | None = None):
+    L = lib()
+    if dtype is None:
+        return getattr(L, name)
+    suffix = {torch.float64: "_f64", torch.float32: "_f32"}.get(dtype)
+    if suffix is None:
+        raise ValueError(f"unsupported dtype {dtype}; use float64 or float32")
+    return getattr(L, name + suffix)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = lib().fmgsr_last_error().decode(errors="replace")
+    if rc == -1:
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, dtype, *args) -> None:
+    check(fn(name, dtype)(*args), name)
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream

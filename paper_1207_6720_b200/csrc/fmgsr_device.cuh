@@ -1,0 +1,342 @@
+// fmgsr_device.cuh -- device building blocks of the FMG-FAS-SR hot path.
+//
+// Layout: every level field is a row-major [n][ld] array, cell index i major,
+// right-hand side r fastest (ld >= B).  One warp = one patch x 32 consecutive
+// RHS columns, one lane = one (patch, rhs) Gauss-Seidel chain, so every load
+// and store of a chain step is a coalesced 256 B (fp64) warp access.
+//
+// Arithmetic: every operation goes through the *_rn intrinsics below, so
+// nvcc can never contract a multiply-add into an FMA.  Together with the
+// reference's expression order this makes the CUDA path bit-identical to
+// the reference numba lane (numba compiles without fastmath, no contraction;
+// reference _kernels_numba.py:3-4).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fmgsr {
+
+typedef int64_t i64;
+
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float xadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float xsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float xmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float xdiv(float a, float b) { return __fdiv_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// Gauss-Seidel cell updates, reference _kernels_numba.py:26-35.
+//   interior : resid = f - inv_h2*((2u - uL) - uR), u += (omega*resid)/(2 inv_h2)
+//   i == 0   : resid = f - inv_h2*(3u - uR),        u += (omega*resid)/(3 inv_h2)
+//   i == n-1 : resid = f - inv_h2*(3u - uL),        u += (omega*resid)/(3 inv_h2)
+// The interior divisor 2*4^k is a power of two, so the division is performed
+// as an exact multiply by rdiag = 2^-(2k+1): both are the correctly rounded
+// value of the same real number, hence bit-identical.  The boundary divisor
+// 3*4^k is not a power of two and stays a true IEEE division.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct GsCoef {
+  T inv_h2;  // 4^k
+  T rdiag;   // 1 / (2 * 4^k), exact
+  T diag_b;  // 3 * 4^k
+  T omega;
+};
+
+template <typename T>
+__device__ __forceinline__ T gs_int(const GsCoef<T>& c, T uL, T u, T uR, T f) {
+  T s = xsub(xsub(xmul(T(2), u), uL), uR);
+  T resid = xsub(f, xmul(c.inv_h2, s));
+  return xadd(u, xmul(xmul(c.omega, resid), c.rdiag));
+}
+
+template <typename T>
+__device__ __forceinline__ T gs_bnd(const GsCoef<T>& c, T u, T nb, T f) {
+  T s = xsub(xmul(T(3), u), nb);
+  T resid = xsub(f, xmul(c.inv_h2, s));
+  return xadd(u, xdiv(xmul(c.omega, resid), c.diag_b));
+}
+
+// One GS update of cell i in a level of n cells (domain rows first, as the
+// reference tests i == 0 before i == n-1).
+template <typename T>
+__device__ __forceinline__ T gs_cell(const GsCoef<T>& c, i64 i, i64 n, T uL, T u, T uR,
+                                     T f) {
+  if (i == 0) return gs_bnd(c, u, uR, f);
+  if (i == n - 1) return gs_bnd(c, u, uL, f);
+  return gs_int(c, uL, u, uR, f);
+}
+
+// Kaczmarz projection of one pair onto its coarse value, reference
+// _kernels_numba.py:53-56: r = uc - 0.5(a+b); t = r/proj_diag; a,b += 0.5 t.
+template <typename T>
+__device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, T proj_diag) {
+  T r = xsub(uc, xmul(T(0.5), xadd(a, b)));
+  T t = xdiv(r, proj_diag);
+  T h = xmul(T(0.5), t);
+  a = xadd(a, h);
+  b = xadd(b, h);
+}
+
+// ---------------------------------------------------------------------------
+// Pair sources: produce the smoother input u_in at fine cells (2q, 2q+1)
+// together with f there, streaming in increasing q.
+//   SRC_LOAD : u_in = u                                   (plain load)
+//   SRC_CORR : u_in = u + P(uH - R u)   reference cycles.py:120-121,
+//              stencils.py:39-64 (restrict, prolong_correction)
+//   SRC_FMG  : u_in = Pi(uH)            reference stencils.py:67-105
+// With CR the pair is projected (Kaczmarz) when it lies in the patch's pair
+// range [ws//2, we//2): exactly the pairs the reference kaczmarz_sweep visits
+// before the GS pass (_kernels_numba.py:42-57, 87-89), applied just in time.
+// Loads are split (load(): raw global reads, no dependencies) from make()
+// (arithmetic + sliding window) so the caller can prefetch raws ahead.
+// ---------------------------------------------------------------------------
+enum { SRC_LOAD = 0, SRC_CORR = 1, SRC_FMG = 2 };
+
+template <typename T>
+struct Raw {
+  T a0, a1, h, g, f0, f1;
+};
+
+template <typename T, int SRC, bool CR>
+struct PairSource {
+  const T* u;   // fine field, column-offset (LOAD, CORR)
+  const T* uH;  // coarse field (CORR, FMG; CR target for FMG)
+  const T* uc;  // CR target for LOAD / CORR
+  const T* f;   // level right-hand side
+  i64 ld, nc;   // row stride, number of pairs (= coarse cells)
+  T proj_diag;
+  i64 wlo, whi;  // Kaczmarz pair range
+  T s0, s1, s2, s3;
+
+  __device__ __forceinline__ i64 cl(i64 q) const { return q < 0 ? 0 : (q >= nc ? nc - 1 : q); }
+
+  __device__ __forceinline__ Raw<T> load(i64 q) const {
+    Raw<T> r;
+    i64 qq = cl(q);
+    r.f0 = ldg(f + (2 * qq) * ld);
+    r.f1 = ldg(f + (2 * qq + 1) * ld);
+    if (SRC == SRC_LOAD) {
+      r.a0 = ldg(u + (2 * qq) * ld);
+      r.a1 = ldg(u + (2 * qq + 1) * ld);
+      r.h = T(0);
+    } else if (SRC == SRC_CORR) {
+      i64 q1 = cl(q + 1);
+      r.a0 = ldg(u + (2 * q1) * ld);
+      r.a1 = ldg(u + (2 * q1 + 1) * ld);
+      r.h = ldg(uH + q1 * ld);
+    } else {
+      r.a0 = r.a1 = T(0);
+      r.h = ldg(uH + cl(q + 2) * ld);
+    }
+    if (CR && SRC != SRC_FMG) r.g = ldg(uc + qq * ld);
+    else r.g = T(0);
+    return r;
+  }
+
+  // sliding-window state before make(q)
+  __device__ __forceinline__ void init(i64 q) {
+    if (SRC == SRC_CORR) {
+      // s0 = c_{q-1}, s1 = c_q, s2 = u[2q], s3 = u[2q+1]; c_j = uH[j] - 0.5(u[2j] + u[2j+1])
+      s2 = ldg(u + (2 * q) * ld);
+      s3 = ldg(u + (2 * q + 1) * ld);
+      s1 = xsub(ldg(uH + q * ld), xmul(T(0.5), xadd(s2, s3)));
+      if (q >= 1) {
+        T a = ldg(u + (2 * q - 2) * ld), b = ldg(u + (2 * q - 1) * ld);
+        s0 = xsub(ldg(uH + (q - 1) * ld), xmul(T(0.5), xadd(a, b)));
+      } else {
+        s0 = T(0);
+      }
+    } else if (SRC == SRC_FMG) {
+      // s0..s3 = c[q-2], c[q-1], c[q], c[q+1] (clamped; boundary rows ignore them)
+      s0 = ldg(uH + cl(q - 2) * ld);
+      s1 = ldg(uH + cl(q - 1) * ld);
+      s2 = ldg(uH + cl(q) * ld);
+      s3 = ldg(uH + cl(q + 1) * ld);
+    }
+  }
+
+  __device__ __forceinline__ void make(i64 q, const Raw<T>& r, T& v0, T& v1) {
+    T target = r.g;
+    if (SRC == SRC_LOAD) {
+      v0 = r.a0;
+      v1 = r.a1;
+    } else if (SRC == SRC_CORR) {
+      T c1 = xsub(r.h, xmul(T(0.5), xadd(r.a0, r.a1)));  // c_{q+1}
+      T p0 = (q == 0) ? xmul(T(0.5), s1) : xmul(T(0.25), xadd(s0, xmul(T(3), s1)));
+      T p1 = (q == nc - 1) ? xmul(T(0.5), s1) : xmul(T(0.25), xadd(xmul(T(3), s1), c1));
+      v0 = xadd(s2, p0);
+      v1 = xadd(s3, p1);
+      s0 = s1;
+      s1 = c1;
+      s2 = r.a0;
+      s3 = r.a1;
+    } else {
+      // prolong_fmg rows, reference stencils.py:85-104 (left-to-right sums, then /128)
+      const T c0 = s0, c1 = s1, c2 = s2, c3 = s3, c4 = r.h;  // c[q-2 .. q+2]
+      T e, o;
+      if (q >= 2 && q <= nc - 3) {
+        e = xsub(xadd(xadd(xmul(T(-5), c0), xmul(T(35), c1)), xmul(T(105), c2)), xmul(T(7), c3));
+        o = xsub(xadd(xadd(xmul(T(-7), c1), xmul(T(105), c2)), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == 0) {  // rows 0, 1 over c[0..2] = c2, c3, c4
+        e = xsub(xmul(T(70), c2), xmul(T(2), c3));
+        o = xsub(xadd(xmul(T(112), c2), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == 1) {  // rows 2, 3 over c[0..3] = c1..c4
+        e = xsub(xadd(xmul(T(40), c1), xmul(T(105), c2)), xmul(T(7), c3));
+        o = xsub(xadd(xadd(xmul(T(-7), c1), xmul(T(105), c2)), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == nc - 2) {  // rows nf-4, nf-3; c[n-1]=c3, c[n-2]=c2, c[n-3]=c1, c[n-4]=c0
+        e = xsub(xadd(xadd(xmul(T(-7), c3), xmul(T(105), c2)), xmul(T(35), c1)), xmul(T(5), c0));
+        o = xsub(xadd(xmul(T(40), c3), xmul(T(105), c2)), xmul(T(7), c1));
+      } else {  // q == nc-1: rows nf-2, nf-1; c[n-1]=c2, c[n-2]=c1, c[n-3]=c0
+        e = xsub(xadd(xmul(T(112), c2), xmul(T(35), c1)), xmul(T(5), c0));
+        o = xsub(xmul(T(70), c2), xmul(T(2), c1));
+      }
+      v0 = xdiv(e, T(128));
+      v1 = xdiv(o, T(128));
+      target = c2;
+      s0 = c1;
+      s1 = c2;
+      s2 = c3;
+      s3 = c4;
+    }
+    if (CR && q >= wlo && q < whi) kaczmarz_pair(v0, v1, target, proj_diag);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Restriction + tau epilogue, fused into the patch chain (reference
+// stencils.py:108-125 coarse_rhs = R f + (L_H R u - R L u), cycles.py:101-102).
+// The chain pushes its smoothed owned pairs in order; coarse cell j-1 is
+// emitted one pair late (it needs R u at j).  The patch's first and last
+// coarse cells need two smoothed fine cells of the neighbouring patch: they
+// are completed by whichever of the two neighbour warps finishes second
+// (edge records + a parity counter, see edge_arrive).  Requires W >= 4.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct EdgeRec {
+  T v[5];
+};
+
+template <typename T>
+struct Epilogue {
+  T inv_h2, inv_H2;
+  bool left_dom, right_dom, write_uH;
+  T* uH_out;  // column-offset
+  T* fH_out;  // column-offset
+  i64 ld, nc;
+  T up2, up1, Lprev, Rm2, Rm1, Rfm1;
+  EdgeRec<T> left;  // u[os], u[os+1], Lu[os+1], Ru_{j0+1}, Rf_{j0}
+  int cnt;
+
+  __device__ __forceinline__ void push(i64 j, T a, T b, T f0, T f1, bool store) {
+    T Rj = xmul(T(0.5), xadd(a, b));
+    T Rfj = xmul(T(0.5), xadd(f0, f1));
+    if (write_uH && store) uH_out[j * ld] = Rj;
+    if (cnt == 0) {
+      if (left_dom) {
+        Lprev = xmul(xsub(xmul(T(3), a), b), inv_h2);  // Lu[0]
+      } else {
+        left.v[0] = a;
+        left.v[1] = b;
+        left.v[4] = Rfj;
+      }
+    } else {
+      T Lodd = xmul(xsub(xsub(xmul(T(2), up1), up2), a), inv_h2);  // Lu[2j-1]
+      if (cnt == 1 && !left_dom) {
+        left.v[2] = Lodd;  // Lu[os+1]
+        left.v[3] = Rj;    // Ru_{j0+1}
+      } else {
+        T RL = xmul(T(0.5), xadd(Lprev, Lodd));
+        T LH = (j - 1 == 0) ? xmul(xsub(xmul(T(3), Rm1), Rj), inv_H2)
+                            : xmul(xsub(xsub(xmul(T(2), Rm1), Rm2), Rj), inv_H2);
+        if (store) fH_out[(j - 1) * ld] = xadd(Rfm1, xsub(LH, RL));
+      }
+      Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);  // Lu[2j]
+    }
+    up2 = a;
+    up1 = b;
+    Rm2 = Rm1;
+    Rm1 = Rj;
+    Rfm1 = Rfj;
+    cnt++;
+  }
+
+  // after the last owned pair: close the domain end or build the right record
+  __device__ __forceinline__ void finish(bool store, EdgeRec<T>& right) {
+    if (right_dom) {
+      T Llast = xmul(xsub(xmul(T(3), up1), up2), inv_h2);  // Lu[n-1]
+      T RL = xmul(T(0.5), xadd(Lprev, Llast));
+      T LH = xmul(xsub(xmul(T(3), Rm1), Rm2), inv_H2);
+      if (store) fH_out[(nc - 1) * ld] = xadd(Rfm1, xsub(LH, RL));
+    } else {
+      right.v[0] = up2;    // u[s-2]
+      right.v[1] = up1;    // u[s-1]
+      right.v[2] = Lprev;  // Lu[s-2]
+      right.v[3] = Rm2;    // Ru_{jL-1}
+      right.v[4] = Rfm1;   // Rf_{jL}
+    }
+  }
+};
+
+// Complete coarse cells s/2-1 and s/2 of the patch boundary at fine cell s
+// from the left record (slots 0-4) and the right record (slots 5-9).
+template <typename T>
+__device__ __forceinline__ void edge_finish(const T* L, const T* R, T inv_h2, T inv_H2, T& fL,
+                                            T& fR) {
+  const T um2 = L[0], um1 = L[1], Lm2 = L[2], RuLm1 = L[3], RfL = L[4];
+  const T u0 = R[0], u1 = R[1], L1 = R[2], RuRp1 = R[3], RfR = R[4];
+  T Lm1 = xmul(xsub(xsub(xmul(T(2), um1), um2), u0), inv_h2);
+  T L0 = xmul(xsub(xsub(xmul(T(2), u0), um1), u1), inv_h2);
+  T RuL = xmul(T(0.5), xadd(um2, um1));
+  T RuR = xmul(T(0.5), xadd(u0, u1));
+  T RLL = xmul(T(0.5), xadd(Lm2, Lm1));
+  T RLR = xmul(T(0.5), xadd(L0, L1));
+  T LHL = xmul(xsub(xsub(xmul(T(2), RuL), RuLm1), RuR), inv_H2);
+  T LHR = xmul(xsub(xsub(xmul(T(2), RuR), RuL), RuRp1), inv_H2);
+  fL = xadd(RfL, xsub(LHL, RLL));
+  fR = xadd(RfR, xsub(LHR, RLR));
+}
+
+// Edge protocol for one boundary (index bi, boundary fine cell s).  Each of
+// the two neighbour warps writes its 5-slot record, fences, and bumps the
+// boundary's counter; the warp that sees an odd old value arrived second and
+// finishes both coarse cells.  Every boundary receives exactly two arrivals
+// per visit, so the parity test stays valid across visits without resets.
+template <typename T>
+__device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i64 bi, int side,
+                                            const EdgeRec<T>& rec, int lane, int rg, int r,
+                                            bool store, T* fH, i64 ld, i64 s, T inv_h2,
+                                            T inv_H2) {
+  T* mine = E + (bi * 10 + side * 5) * ldE + r;
+#pragma unroll
+  for (int k = 0; k < 5; k++) mine[k * ldE] = rec.v[k];
+  __threadfence();
+  __syncwarp();
+  int old = 0;
+  if (lane == 0) old = atomicAdd(cnt + bi * nrg + rg, 1);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old & 1) {
+    __threadfence();
+    const T* base = E + bi * 10 * ldE + r;
+    T Lr[5], Rr[5];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+      Lr[k] = __ldcg(base + k * ldE);
+      Rr[k] = __ldcg(base + (5 + k) * ldE);
+    }
+    T fL, fR;
+    edge_finish(Lr, Rr, inv_h2, inv_H2, fL, fR);
+    if (store) {
+      fH[(s / 2 - 1) * ld] = fL;
+      fH[(s / 2) * ld] = fR;
+    }
+  }
+}
+
+}  // namespace fmgsr

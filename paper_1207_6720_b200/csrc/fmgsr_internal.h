@@ -1,0 +1,130 @@
+// fmgsr_internal.h -- host-side internals shared by the translation units of
+// libfmgsr_cuda.so: error reporting for the C ABI and the launcher templates.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace fmgsr {
+
+typedef int64_t i64;
+
+// Thrown by launchers and validators; turned into a negative return code and
+// the text behind fmgsr_last_error() at the C-ABI boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+enum { ERR_ARG = -1, ERR_CUDA = -2, ERR_INTERNAL = -3 };
+
+void set_last_error(const std::string& msg);
+void clear_last_error();
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+inline void check_launch(const char* what) { check_cuda(cudaGetLastError(), what); }
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(ERR_ARG, msg);
+}
+
+inline int level_of(i64 n) {
+  int k = 0;
+  while (((i64)1 << (k + 1)) <= n) k++;
+  return k;
+}
+inline bool is_pow2(i64 n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+// Run f(); map exceptions to C return codes.
+template <typename F>
+int guarded(F&& f) {
+  try {
+    clear_last_error();
+    f();
+    return 0;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return ERR_INTERNAL;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level-visit descriptor (uniform patch geometry: owned width W, buffer b).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct VisitDesc {
+  int src = 0;  // SRC_LOAD / SRC_CORR / SRC_FMG
+  bool cr = false, epi = false, write_u = true;
+  i64 n = 0, ld = 0;
+  int B = 0;
+  i64 W = 0, b = 0;
+  double omega = 1.0, proj_diag = 0.5;
+  const T* u_src = nullptr;  // fine input (LOAD, CORR)
+  const T* uH = nullptr;     // coarse input (CORR, FMG, CR target)
+  const T* uc = nullptr;     // CR target for LOAD / CORR
+  const T* f = nullptr;
+  T* u_out = nullptr;
+  T* uH_out = nullptr;  // epilogue
+  T* fH_out = nullptr;
+  T* E = nullptr;    // edge records
+  int* cnt = nullptr;  // edge counters
+  // explicit patch arrays (optional; SRC_LOAD, no epilogue)
+  const i64* olo = nullptr;
+  const i64* ohi = nullptr;
+  const i64* elo = nullptr;
+  const i64* ehi = nullptr;
+  i64 P = 0;  // number of patches when arrays are given
+};
+
+template <typename T>
+void launch_visit(const VisitDesc<T>& d, cudaStream_t s);
+
+// Any ns (window staged in a per-chain global scratch).
+template <typename T>
+struct ScratchDesc {
+  i64 n = 0, ld = 0;
+  int B = 0;
+  i64 W = 0, b = 0;  // uniform geometry when olo == nullptr
+  const i64* olo = nullptr;
+  const i64* ohi = nullptr;
+  const i64* elo = nullptr;
+  const i64* ehi = nullptr;
+  const i64* soff = nullptr;  // per-patch scratch row offset (arrays mode)
+  i64 P = 0;
+  i64 ns = 1;
+  double omega = 1.0, proj_diag = 0.5;
+  const T* u_in = nullptr;
+  const T* f = nullptr;
+  const T* uc = nullptr;  // non-null => CR
+  T* out = nullptr;
+  T* scratch = nullptr;
+  i64 sld = 0;  // scratch row stride (>= round_up(B, 32))
+};
+
+template <typename T>
+void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s);
+inline i64 scratch_rows_uniform(i64 n, i64 W, i64 b) { return (n / W) * (W + 2 * b + 2); }
+
+// Stencil / level operators ([n][ld] layout, B active columns).
+template <typename T> void launch_apply_operator(const T* u, T* out, i64 n, i64 ld, int B, cudaStream_t s);
+template <typename T> void launch_restrict(const T* u, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
+template <typename T> void launch_prolong_correction(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s);
+template <typename T> void launch_prolong_fmg(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s);
+// mode 0: tau only; 1: coarse_rhs; 2: restrict + coarse_rhs (uH_out, fH_out)
+template <typename T> void launch_restrict_tau(const T* u, const T* f, T* uH_out, T* fH_out, i64 nf, i64 ld, int B, int mode, cudaStream_t s);
+template <typename T> void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
+template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s, T* workspace = nullptr);
+template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);
+template <typename T> void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop, double proj_diag, cudaStream_t s);
+template <typename T> void launch_fourier_rhs(const double* coef, int K, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
+template <typename T> void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
+
+}  // namespace fmgsr

@@ -1,0 +1,432 @@
+// kernels_ops.cu -- level operators and single-purpose kernels.
+//
+// Elementwise stencils over [n][ld] fields (block 32 x 8: lanes along the RHS
+// columns, so each warp access is coalesced), the coarsest-level direct
+// solve, the windowed Gauss-Seidel and Kaczmarz sweeps of the lane API, and
+// the synthetic right-hand-side generators.  All arithmetic is exact-order
+// (no contraction), matching the reference numpy/numba expressions cited.
+#include <cmath>
+
+#include "fmgsr_device.cuh"
+#include "fmgsr_internal.h"
+
+namespace fmgsr {
+
+namespace {
+
+constexpr int TX = 32, TY = 8;
+
+inline dim3 grid_for(i64 rows, int B) {
+  i64 gy = (rows + TY - 1) / TY;
+  if (gy > 32768) gy = 32768;
+  if (gy < 1) gy = 1;
+  return dim3((unsigned)((B + TX - 1) / TX), (unsigned)gy);
+}
+
+#define ROWS_LOOP(i, rows) \
+  for (i64 i = (i64)blockIdx.y * TY + threadIdx.y; i < (rows); i += (i64)gridDim.y * TY)
+
+template <typename T>
+__device__ __forceinline__ T inv_h2_of(i64 n) {
+  int k = 0;
+  while (((i64)1 << (k + 1)) <= n) k++;
+  return (T)(double)((i64)1 << (2 * k));
+}
+
+// stencils.py:27-36
+template <typename T>
+__device__ __forceinline__ T lu_at(const T* u, i64 i, i64 n, i64 ld, T ih) {
+  T s;
+  if (i == 0) s = xsub(xmul(T(3), u[0]), u[ld]);
+  else if (i == n - 1) s = xsub(xmul(T(3), u[(n - 1) * ld]), u[(n - 2) * ld]);
+  else s = xsub(xsub(xmul(T(2), u[i * ld]), u[(i - 1) * ld]), u[(i + 1) * ld]);
+  return xmul(s, ih);
+}
+
+template <typename T>
+__device__ __forceinline__ T ru_at(const T* u, i64 j, i64 ld) {
+  return xmul(T(0.5), xadd(u[(2 * j) * ld], u[(2 * j + 1) * ld]));
+}
+
+template <typename T>
+__global__ void k_apply_operator(const T* __restrict__ u, T* __restrict__ out, i64 n, i64 ld, int B) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  T ih = inv_h2_of<T>(n);
+  ROWS_LOOP(i, n) out[i * ld + r] = lu_at(u + r, i, n, ld, ih);
+}
+
+// stencils.py:39-47
+template <typename T>
+__global__ void k_restrict(const T* __restrict__ u, T* __restrict__ out, i64 nf, i64 ld, int B) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  ROWS_LOOP(j, nf / 2) out[j * ld + r] = ru_at(u + r, j, ld);
+}
+
+// stencils.py:50-64
+template <typename T>
+__device__ __forceinline__ T pc_at(const T* c, i64 i, i64 nc, i64 ld) {
+  i64 nf = 2 * nc;
+  if (i == 0) return xmul(T(0.5), c[0]);
+  if (i == nf - 1) return xmul(T(0.5), c[(nc - 1) * ld]);
+  if (i & 1) {
+    i64 j = (i - 1) / 2;
+    return xmul(T(0.25), xadd(xmul(T(3), c[j * ld]), c[(j + 1) * ld]));
+  }
+  i64 j = (i - 2) / 2;
+  return xmul(T(0.25), xadd(c[j * ld], xmul(T(3), c[(j + 1) * ld])));
+}
+
+template <typename T>
+__global__ void k_prolong_correction(const T* __restrict__ c, T* __restrict__ out, i64 nc, i64 ld,
+                                     int B) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  ROWS_LOOP(i, 2 * nc) out[i * ld + r] = pc_at(c + r, i, nc, ld);
+}
+
+// stencils.py:67-105 (one fine row)
+template <typename T>
+__device__ __forceinline__ T pf_at(const T* c, i64 i, i64 n, i64 ld) {
+  i64 nf = 2 * n;
+#define C(k) c[(k) * ld]
+  T v;
+  if (i == 0) v = xsub(xmul(T(70), C(0)), xmul(T(2), C(1)));
+  else if (i == 1) v = xsub(xadd(xmul(T(112), C(0)), xmul(T(35), C(1))), xmul(T(5), C(2)));
+  else if (i == 2) v = xsub(xadd(xmul(T(40), C(0)), xmul(T(105), C(1))), xmul(T(7), C(2)));
+  else if (i == 3)
+    v = xsub(xadd(xadd(xmul(T(-7), C(0)), xmul(T(105), C(1))), xmul(T(35), C(2))), xmul(T(5), C(3)));
+  else if (i == nf - 4)
+    v = xsub(xadd(xadd(xmul(T(-7), C(n - 1)), xmul(T(105), C(n - 2))), xmul(T(35), C(n - 3))),
+             xmul(T(5), C(n - 4)));
+  else if (i == nf - 3)
+    v = xsub(xadd(xmul(T(40), C(n - 1)), xmul(T(105), C(n - 2))), xmul(T(7), C(n - 3)));
+  else if (i == nf - 2)
+    v = xsub(xadd(xmul(T(112), C(n - 1)), xmul(T(35), C(n - 2))), xmul(T(5), C(n - 3)));
+  else if (i == nf - 1) v = xsub(xmul(T(70), C(n - 1)), xmul(T(2), C(n - 2)));
+  else if ((i & 1) == 0) {
+    i64 q = i / 2;
+    v = xsub(xadd(xadd(xmul(T(-5), C(q - 2)), xmul(T(35), C(q - 1))), xmul(T(105), C(q))),
+             xmul(T(7), C(q + 1)));
+  } else {
+    i64 q = (i - 1) / 2;
+    v = xsub(xadd(xadd(xmul(T(-7), C(q - 1)), xmul(T(105), C(q))), xmul(T(35), C(q + 1))),
+             xmul(T(5), C(q + 2)));
+  }
+#undef C
+  return xdiv(v, T(128));
+}
+
+template <typename T>
+__global__ void k_prolong_fmg(const T* __restrict__ c, T* __restrict__ out, i64 nc, i64 ld, int B) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  ROWS_LOOP(i, 2 * nc) out[i * ld + r] = pf_at(c + r, i, nc, ld);
+}
+
+// stencils.py:108-125.  mode 0: tau; 1: coarse_rhs; 2: restrict + coarse_rhs.
+template <typename T>
+__global__ void k_restrict_tau(const T* __restrict__ u, const T* __restrict__ f, T* __restrict__ uH,
+                               T* __restrict__ fH, i64 nf, i64 ld, int B, int mode) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  const i64 nc = nf / 2;
+  const T ih = inv_h2_of<T>(nf), iH = inv_h2_of<T>(nc);
+  const T* ur = u + r;
+  ROWS_LOOP(j, nc) {
+    T Rj = ru_at(ur, j, ld);
+    T LH;
+    if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru_at(ur, 1, ld)), iH);
+    else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rj), ru_at(ur, nc - 2, ld)), iH);
+    else LH = xmul(xsub(xsub(xmul(T(2), Rj), ru_at(ur, j - 1, ld)), ru_at(ur, j + 1, ld)), iH);
+    T RL = xmul(T(0.5), xadd(lu_at(ur, 2 * j, nf, ld, ih), lu_at(ur, 2 * j + 1, nf, ld, ih)));
+    T tau = xsub(LH, RL);
+    if (mode == 0) {
+      fH[j * ld + r] = tau;
+    } else {
+      T Rf = ru_at(f + r, j, ld);
+      fH[j * ld + r] = xadd(Rf, tau);
+      if (mode == 2) uH[j * ld + r] = Rj;
+    }
+  }
+}
+
+// cycles.py:120-121: out = u + prolong_correction(uH - restrict(u))
+template <typename T>
+__global__ void k_fas_correct(const T* __restrict__ u, const T* __restrict__ uH, T* __restrict__ out,
+                              i64 nf, i64 ld, int B) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  const i64 nc = nf / 2;
+  const T* ur = u + r;
+  const T* hr = uH + r;
+  ROWS_LOOP(i, nf) {
+    auto c = [&](i64 j) { return xsub(hr[j * ld], ru_at(ur, j, ld)); };
+    T p;
+    if (i == 0) p = xmul(T(0.5), c(0));
+    else if (i == nf - 1) p = xmul(T(0.5), c(nc - 1));
+    else if (i & 1) {
+      i64 j = (i - 1) / 2;
+      p = xmul(T(0.25), xadd(xmul(T(3), c(j)), c(j + 1)));
+    } else {
+      i64 j = (i - 2) / 2;
+      p = xmul(T(0.25), xadd(c(j), xmul(T(3), c(j + 1))));
+    }
+    out[i * ld + r] = xadd(ur[i * ld], p);
+  }
+}
+
+// smoothers.py:210-225 -> scipy solveh_banded -> LAPACK ?ptsv: dpttrf (L D L^T)
+// then dptts2.  The factor depends on n only; pt_factor builds it with the
+// dpttrf operation order (into shared memory per block, or once into a global
+// workspace for large n); pt_solve runs dptts2, one thread per RHS.
+template <typename T>
+__device__ void pt_factor(T* d, T* e, i64 n) {
+  T ih = inv_h2_of<T>(n);
+  for (i64 i = 0; i < n; i++) d[i] = xmul(T(2), ih);
+  d[0] = xmul(T(3), ih);
+  d[n - 1] = xmul(T(3), ih);
+  for (i64 i = 0; i < n - 1; i++) e[i] = -ih;
+  for (i64 i = 0; i < n - 1; i++) {
+    T ei = e[i];
+    e[i] = xdiv(ei, d[i]);
+    d[i + 1] = xsub(d[i + 1], xmul(e[i], ei));
+  }
+}
+
+template <typename T>
+__global__ void k_pt_factor(T* fac, i64 n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) pt_factor(fac, fac + n, n);
+}
+
+template <typename T>
+__global__ void k_direct_solve(const T* __restrict__ f, T* __restrict__ u, i64 n, i64 ld, int B,
+                               const T* __restrict__ fac) {
+  extern __shared__ unsigned char smem_raw[];
+  const T* d;
+  const T* e;
+  if (fac) {
+    d = fac;
+    e = fac + n;
+  } else {
+    T* ds = reinterpret_cast<T*>(smem_raw);
+    if (threadIdx.x == 0) pt_factor(ds, ds + n, n);
+    __syncthreads();
+    d = ds;
+    e = ds + n;
+  }
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  const T* fr = f + r;
+  T* ur = u + r;
+  T prev = fr[0];
+  ur[0] = prev;
+  for (i64 i = 1; i < n; i++) {
+    prev = xsub(fr[i * ld], xmul(prev, e[i - 1]));
+    ur[i * ld] = prev;
+  }
+  T nxt = xdiv(prev, d[n - 1]);
+  ur[(n - 1) * ld] = nxt;
+  for (i64 i = n - 2; i >= 0; i--) {
+    nxt = xsub(xdiv(ur[i * ld], d[i]), xmul(nxt, e[i]));
+    ur[i * ld] = nxt;
+  }
+}
+
+// _kernels_numba.py:15-36, one thread per RHS, in place
+template <typename T>
+__global__ void k_gs_sweep(T* u, const T* __restrict__ f, i64 n, i64 ld, int B, GsCoef<T> gc,
+                           i64 start, i64 stop, bool forward) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  T* ur = u + r;
+  const T* fr = f + r;
+  if (forward) {
+    T uL = start > 0 ? ur[(start - 1) * ld] : T(0);
+    T cur = ur[start * ld];
+    for (i64 i = start; i < stop; i++) {
+      T nxt = (i + 1 < n) ? ur[(i + 1) * ld] : T(0);
+      T v = gs_cell(gc, i, n, uL, cur, nxt, fr[i * ld]);
+      ur[i * ld] = v;
+      uL = v;
+      cur = nxt;
+    }
+  } else {
+    T uR = stop < n ? ur[stop * ld] : T(0);
+    T cur = ur[(stop - 1) * ld];
+    for (i64 i = stop - 1; i >= start; i--) {
+      T prv = i > 0 ? ur[(i - 1) * ld] : T(0);
+      T v = gs_cell(gc, i, n, prv, cur, uR, fr[i * ld]);
+      ur[i * ld] = v;
+      uR = v;
+      cur = prv;
+    }
+  }
+}
+
+// _kernels_numba.py:39-57: disjoint pairs, so every pair is projected
+// independently (the sweep direction cannot change the result).
+template <typename T>
+__global__ void k_kaczmarz(T* u, const T* __restrict__ uc, i64 j0, i64 j1, i64 ld, int B,
+                           T proj_diag) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  ROWS_LOOP(k, j1 - j0) {
+    i64 j = j0 + k;
+    T a = u[(2 * j) * ld + r], b = u[(2 * j + 1) * ld + r];
+    kaczmarz_pair(a, b, uc[j * ld + r], proj_diag);
+    u[(2 * j) * ld + r] = a;
+    u[(2 * j + 1) * ld + r] = b;
+  }
+}
+
+// Synthetic Fourier forcing: f = sum_k a_k sin(k pi x),
+// u* = sum_k a_k sin(k pi x) / (k pi)^2, x_i = (i + 1/2)/n; coef is [B][K].
+template <typename T>
+__global__ void k_fourier_rhs(const double* __restrict__ coef, int K, i64 n, i64 ld, int B, T* f,
+                              T* uex) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  const double* a = coef + (i64)r * K;
+  ROWS_LOOP(i, n) {
+    double x = ((double)i + 0.5) / (double)n;
+    double fs = 0.0, us = 0.0;
+    for (int k = 1; k <= K; k++) {
+      double s = sinpi((double)k * x);
+      double kp = (double)k * M_PI;
+      fs += a[k - 1] * s;
+      us += a[k - 1] * s / (kp * kp);
+    }
+    f[i * ld + r] = (T)fs;
+    if (uex) uex[i * ld + r] = (T)us;
+  }
+}
+
+// Nonlinear manufactured problem (BASELINE config 3): u = s x(1-x)e^x,
+// f = s x(x+3)e^x + (s x(1-x)e^x)^3 for -u'' + u^3 = f.
+template <typename T>
+__global__ void k_nonlinear_rhs(const double* __restrict__ scale, i64 n, i64 ld, int B, T* f,
+                                T* uex) {
+  int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  const double s = scale[r];
+  ROWS_LOOP(i, n) {
+    double x = ((double)i + 0.5) / (double)n;
+    double ex = exp(x);
+    double u = s * x * (1.0 - x) * ex;
+    f[i * ld + r] = (T)(s * x * (x + 3.0) * ex + u * u * u);
+    if (uex) uex[i * ld + r] = (T)u;
+  }
+}
+
+}  // namespace
+
+template <typename T>
+void launch_apply_operator(const T* u, T* out, i64 n, i64 ld, int B, cudaStream_t s) {
+  require(n >= 2 && is_pow2(n), "apply_operator: size must be a power of two >= 2");
+  k_apply_operator<T><<<grid_for(n, B), dim3(TX, TY), 0, s>>>(u, out, n, ld, B);
+  check_launch("apply_operator");
+}
+template <typename T>
+void launch_restrict(const T* u, T* out, i64 nf, i64 ld, int B, cudaStream_t s) {
+  require(nf >= 2 && is_pow2(nf), "restrict: size must be a power of two >= 2");
+  k_restrict<T><<<grid_for(nf / 2, B), dim3(TX, TY), 0, s>>>(u, out, nf, ld, B);
+  check_launch("restrict");
+}
+template <typename T>
+void launch_prolong_correction(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s) {
+  require(nc >= 2 && is_pow2(nc), "prolong_correction: size must be a power of two >= 2");
+  k_prolong_correction<T><<<grid_for(2 * nc, B), dim3(TX, TY), 0, s>>>(c, out, nc, ld, B);
+  check_launch("prolong_correction");
+}
+template <typename T>
+void launch_prolong_fmg(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s) {
+  require(nc >= 4 && is_pow2(nc), "prolong_fmg: coarse size must be a power of two >= 4");
+  k_prolong_fmg<T><<<grid_for(2 * nc, B), dim3(TX, TY), 0, s>>>(c, out, nc, ld, B);
+  check_launch("prolong_fmg");
+}
+template <typename T>
+void launch_restrict_tau(const T* u, const T* f, T* uH, T* fH, i64 nf, i64 ld, int B, int mode,
+                         cudaStream_t s) {
+  require(nf >= 4 && is_pow2(nf), "tau: fine size must be a power of two >= 4");
+  k_restrict_tau<T><<<grid_for(nf / 2, B), dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode);
+  check_launch("restrict_tau");
+}
+template <typename T>
+void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s) {
+  require(nf >= 4 && is_pow2(nf), "fas_correct: fine size must be a power of two >= 4");
+  k_fas_correct<T><<<grid_for(nf, B), dim3(TX, TY), 0, s>>>(u, uH, out, nf, ld, B);
+  check_launch("fas_correct");
+}
+template <typename T>
+void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s, T* workspace) {
+  require(n >= 2 && is_pow2(n), "direct_solve: size must be a power of two >= 2");
+  int threads = 128;
+  if (workspace) {
+    k_pt_factor<T><<<1, 1, 0, s>>>(workspace, n);
+    check_launch("pt_factor");
+    k_direct_solve<T><<<(B + threads - 1) / threads, threads, 0, s>>>(f, u, n, ld, B, workspace);
+  } else {
+    require(n <= 2048, "direct_solve: n > 2048 needs a workspace of 2n elements");
+    size_t smem = 2 * (size_t)n * sizeof(T);
+    k_direct_solve<T><<<(B + threads - 1) / threads, threads, smem, s>>>(f, u, n, ld, B, nullptr);
+  }
+  check_launch("direct_solve");
+}
+template <typename T>
+void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop,
+                     bool forward, double omega, cudaStream_t s) {
+  require(0 <= start && start < stop && stop <= n, "gs_sweep: window outside [0, n)");
+  GsCoef<T> gc;
+  gc.inv_h2 = (T)inv_h2;
+  gc.rdiag = (T)(1.0 / (2.0 * inv_h2));
+  gc.diag_b = (T)(3.0 * inv_h2);
+  gc.omega = (T)omega;
+  // rdiag must be exact: inv_h2 a power of two (true for every level, 4^k)
+  int e;
+  require(std::frexp(inv_h2, &e) == 0.5, "gs_sweep: inv_h2 must be a power of two");
+  k_gs_sweep<T><<<(B + 127) / 128, 128, 0, s>>>(u, f, n, ld, B, gc, start, stop, forward);
+  check_launch("gs_sweep");
+}
+template <typename T>
+void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop,
+                           double proj_diag, cudaStream_t s) {
+  require(0 <= start && start <= stop && stop <= n, "kaczmarz_sweep: window outside [0, n]");
+  i64 j0 = start / 2, j1 = stop / 2;
+  if (j1 <= j0) return;
+  k_kaczmarz<T><<<grid_for(j1 - j0, B), dim3(TX, TY), 0, s>>>(u, uc, j0, j1, ld, B, (T)proj_diag);
+  check_launch("kaczmarz_sweep");
+}
+template <typename T>
+void launch_fourier_rhs(const double* coef, int K, i64 n, i64 ld, int B, T* f, T* uex,
+                        cudaStream_t s) {
+  k_fourier_rhs<T><<<grid_for(n, B), dim3(TX, TY), 0, s>>>(coef, K, n, ld, B, f, uex);
+  check_launch("fourier_rhs");
+}
+template <typename T>
+void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s) {
+  k_nonlinear_rhs<T><<<grid_for(n, B), dim3(TX, TY), 0, s>>>(scale, n, ld, B, f, uex);
+  check_launch("nonlinear_rhs");
+}
+
+#define FMGSR_INST(T)                                                                          \
+  template void launch_apply_operator<T>(const T*, T*, i64, i64, int, cudaStream_t);          \
+  template void launch_restrict<T>(const T*, T*, i64, i64, int, cudaStream_t);                \
+  template void launch_prolong_correction<T>(const T*, T*, i64, i64, int, cudaStream_t);      \
+  template void launch_prolong_fmg<T>(const T*, T*, i64, i64, int, cudaStream_t);             \
+  template void launch_restrict_tau<T>(const T*, const T*, T*, T*, i64, i64, int, int,        \
+                                       cudaStream_t);                                          \
+  template void launch_fas_correct<T>(const T*, const T*, T*, i64, i64, int, cudaStream_t);   \
+  template void launch_direct_solve<T>(const T*, T*, i64, i64, int, cudaStream_t, T*);            \
+  template void launch_gs_sweep<T>(T*, const T*, i64, i64, int, double, i64, i64, bool,       \
+                                   double, cudaStream_t);                                      \
+  template void launch_kaczmarz_sweep<T>(T*, const T*, i64, i64, int, i64, i64, double,       \
+                                         cudaStream_t);                                        \
+  template void launch_fourier_rhs<T>(const double*, int, i64, i64, int, T*, T*, cudaStream_t); \
+  template void launch_nonlinear_rhs<T>(const double*, i64, i64, int, T*, T*, cudaStream_t);
+FMGSR_INST(double)
+FMGSR_INST(float)
+#undef FMGSR_INST
+
+}  // namespace fmgsr

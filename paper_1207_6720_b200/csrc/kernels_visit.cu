@@ -1,0 +1,322 @@
+// kernels_visit.cu -- the patch-sweep kernels.
+//
+// visit_kernel: one warp per (patch, 32 RHS), one lane per chain.  Fuses the
+// level visit of the FMG cycle (reference cycles.py:187-199, 95-134):
+//   prologue  : u_in from LOAD / FAS correction / FMG prolongation (+CR)
+//   smoother  : additive patch Gauss-Seidel, ns = 1 (_kernels_numba.py:60-92)
+//   epilogue  : owned store, and optionally restriction + tau for the next
+//               coarser level (stencils.py:39-47, 108-125) with the patch-
+//               boundary coarse cells completed by the second-arriving warp.
+// smooth_scratch_kernel: any ns; the extended window is staged per chain in
+// a global scratch and replayed exactly as the reference does (Kaczmarz
+// pass, GS pass, direction flip per repetition, owned write-back).
+#include "fmgsr_chain.cuh"
+#include "fmgsr_internal.h"
+
+namespace fmgsr {
+
+template <typename T>
+struct VisitArgs {
+  i64 n, ld, W, b, P, nc;
+  int B, nrg;
+  GsCoef<T> gc;
+  T inv_H2, proj_diag;
+  bool write_u;
+  const T *u_src, *uH, *uc, *f;
+  T *u_out, *uH_out, *fH_out, *E;
+  int* cnt;
+  const i64 *olo, *ohi, *elo, *ehi;
+};
+
+template <typename T, int SRC, bool CR, bool EPI>
+__global__ void __launch_bounds__(128) visit_kernel(const VisitArgs<T> a) {
+  const int lane = threadIdx.x & 31;
+  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 p = gw / a.nrg;
+  const int rg = (int)(gw - p * a.nrg);
+  if (p >= a.P) return;  // warp-uniform
+  const int r = rg * 32 + lane;
+  const bool store = r < a.B;
+  const int rr = store ? r : a.B - 1;
+
+  i64 os, oe, ws, we;
+  if (a.olo) {
+    os = a.olo[p];
+    oe = a.ohi[p];
+    ws = a.elo[p];
+    we = a.ehi[p];
+  } else {
+    os = p * a.W;
+    oe = os + a.W;
+    ws = os - a.b > 0 ? os - a.b : 0;
+    we = oe + a.b < a.n ? oe + a.b : a.n;
+  }
+
+  PairSource<T, SRC, CR> src;
+  src.u = a.u_src ? a.u_src + rr : nullptr;
+  src.uH = a.uH ? a.uH + rr : nullptr;
+  src.uc = a.uc ? a.uc + rr : nullptr;
+  src.f = a.f + rr;
+  src.ld = a.ld;
+  src.nc = a.nc;
+  src.proj_diag = a.proj_diag;
+  src.wlo = ws >> 1;
+  src.whi = we >> 1;
+
+  T* out = a.u_out ? a.u_out + r : nullptr;
+  if (!EPI) {
+    run_chain_ns1<T, SRC, CR, false>(src, a.gc, a.n, ws, os, oe, out, a.ld, true, store, nullptr);
+    return;
+  }
+  Epilogue<T> ep;
+  ep.inv_h2 = a.gc.inv_h2;
+  ep.inv_H2 = a.inv_H2;
+  ep.left_dom = (os == 0);
+  ep.right_dom = (oe == a.n);
+  ep.write_uH = a.uH_out != nullptr;
+  ep.uH_out = a.uH_out ? a.uH_out + r : nullptr;
+  ep.fH_out = a.fH_out + r;
+  ep.ld = a.ld;
+  ep.nc = a.nc;
+  ep.cnt = 0;
+  ep.up2 = ep.up1 = ep.Lprev = ep.Rm2 = ep.Rm1 = ep.Rfm1 = T(0);
+  run_chain_ns1<T, SRC, CR, true>(src, a.gc, a.n, ws, os, oe, out, a.ld, a.write_u, store, &ep);
+  EdgeRec<T> right;
+  ep.finish(store, right);
+  const i64 ldE = (i64)a.nrg * 32;
+  if (!ep.left_dom)
+    edge_arrive(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, a.ld, os,
+                ep.inv_h2, ep.inv_H2);
+  if (!ep.right_dom)
+    edge_arrive(a.E, a.cnt, ldE, a.nrg, p + 1, 0, right, lane, rg, r, store, ep.fH_out, a.ld, oe,
+                ep.inv_h2, ep.inv_H2);
+}
+
+template <typename T>
+static GsCoef<T> make_coef(i64 n, double omega) {
+  int k = level_of(n);
+  GsCoef<T> g;
+  double inv_h2 = (double)((i64)1 << (2 * k));
+  g.inv_h2 = (T)inv_h2;
+  g.rdiag = (T)(1.0 / (2.0 * inv_h2));  // exact power of two
+  g.diag_b = (T)(3.0 * inv_h2);
+  g.omega = (T)omega;
+  return g;
+}
+
+template <typename T, int SRC, bool CR, bool EPI>
+static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
+  i64 warps = a.P * a.nrg;
+  i64 blocks = (warps + 3) / 4;
+  visit_kernel<T, SRC, CR, EPI><<<(unsigned)blocks, 128, 0, s>>>(a);
+}
+
+template <typename T>
+void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
+  require(d.n >= 2 && is_pow2(d.n), "visit: level size must be a power of two >= 2");
+  require(d.B >= 1 && d.ld >= d.B, "visit: need 1 <= B <= ld");
+  require(d.f != nullptr, "visit: f is null");
+  VisitArgs<T> a;
+  a.n = d.n;
+  a.ld = d.ld;
+  a.B = d.B;
+  a.nrg = (d.B + 31) / 32;
+  a.nc = d.n / 2;
+  a.gc = make_coef<T>(d.n, d.omega);
+  a.inv_H2 = (T)(double)((i64)1 << (2 * (level_of(d.n) - 1)));
+  a.proj_diag = (T)d.proj_diag;
+  a.write_u = d.write_u;
+  a.u_src = d.u_src;
+  a.uH = d.uH;
+  a.uc = d.uc;
+  a.f = d.f;
+  a.u_out = d.u_out;
+  a.uH_out = d.uH_out;
+  a.fH_out = d.fH_out;
+  a.E = d.E;
+  a.cnt = d.cnt;
+  a.olo = d.olo;
+  a.ohi = d.ohi;
+  a.elo = d.elo;
+  a.ehi = d.ehi;
+  if (d.olo) {
+    require(d.src == SRC_LOAD && !d.epi, "visit: patch arrays only with plain loads");
+    a.P = d.P;
+    a.W = 0;
+    a.b = 0;
+  } else {
+    require(d.W >= 2 && d.W % 2 == 0 && d.n % d.W == 0, "visit: owned width must be even and divide n");
+    require(d.b >= 0, "visit: negative buffer");
+    a.W = d.W;
+    a.b = d.b;
+    a.P = d.n / d.W;
+  }
+  if (d.src == SRC_LOAD) require(d.u_src != nullptr, "visit: LOAD needs u_src");
+  if (d.src == SRC_CORR) require(d.u_src && d.uH, "visit: CORR needs u_src and uH");
+  if (d.src == SRC_FMG) require(d.uH && d.n >= 8, "visit: FMG needs uH with >= 4 coarse cells");
+  if (d.cr && d.src != SRC_FMG) require(d.uc != nullptr, "visit: CR needs uc");
+  if (d.epi) {
+    require(d.W >= 4 && d.n >= 8, "visit: fused restriction needs owned width >= 4");
+    require(d.fH_out && d.E && d.cnt, "visit: epilogue buffers missing");
+  } else {
+    require(d.u_out != nullptr, "visit: u_out is null");
+  }
+  if (a.P == 0) return;
+#define FMGSR_DISPATCH(SRCV)                                                    \
+  if (d.cr) {                                                                  \
+    if (d.epi) launch_visit_t<T, SRCV, true, true>(a, s);                      \
+    else launch_visit_t<T, SRCV, true, false>(a, s);                           \
+  } else {                                                                     \
+    if (d.epi) launch_visit_t<T, SRCV, false, true>(a, s);                     \
+    else launch_visit_t<T, SRCV, false, false>(a, s);                          \
+  }
+  if (d.src == SRC_LOAD) {
+    FMGSR_DISPATCH(SRC_LOAD)
+  } else if (d.src == SRC_CORR) {
+    FMGSR_DISPATCH(SRC_CORR)
+  } else {
+    FMGSR_DISPATCH(SRC_FMG)
+  }
+#undef FMGSR_DISPATCH
+  check_launch("visit_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Any-ns smoother with a staged window (reference _kernels_numba.py:60-92 in
+// its literal form).  Scratch layout: [row][sld], one column per chain lane,
+// patch p owning rows soff(p) .. soff(p) + (hi - lo).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct ScratchArgs {
+  i64 n, ld, W, b, P, ns, sld;
+  int B, nrg;
+  GsCoef<T> gc;
+  T proj_diag;
+  const i64 *olo, *ohi, *elo, *ehi, *soff;
+  const T *u_in, *f, *uc;
+  T *out, *scratch;
+};
+
+template <typename T, bool CR>
+__global__ void __launch_bounds__(128) smooth_scratch_kernel(const ScratchArgs<T> a) {
+  const int lane = threadIdx.x & 31;
+  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 p = gw / a.nrg;
+  const int rg = (int)(gw - p * a.nrg);
+  if (p >= a.P) return;
+  const int r = rg * 32 + lane;
+  const bool store = r < a.B;
+  const int rr = store ? r : a.B - 1;
+  i64 os, oe, ws, we, off;
+  if (a.olo) {
+    os = a.olo[p];
+    oe = a.ohi[p];
+    ws = a.elo[p];
+    we = a.ehi[p];
+    off = a.soff[p];
+  } else {
+    os = p * a.W;
+    oe = os + a.W;
+    ws = os - a.b > 0 ? os - a.b : 0;
+    we = oe + a.b < a.n ? oe + a.b : a.n;
+    off = p * (a.W + 2 * a.b + 2);
+  }
+  const i64 n = a.n, ld = a.ld;
+  const i64 lo = ws > 0 ? ws - 1 : 0;
+  const i64 hi = we < n ? we + 1 : n;
+  T* S0 = a.scratch + off * a.sld + r;  // window cell i lives at S0[(i - lo) * sld]
+  const i64 sld = a.sld;
+#define S(i) S0[((i) - lo) * sld]
+  const T* f = a.f + rr;
+  const T* ui = a.u_in + rr;
+  for (i64 i = lo; i < hi; i++) S(i) = ldg(ui + i * ld);
+  bool forward = true;
+  for (i64 rep = 0; rep < a.ns; rep++) {
+    if (CR) {
+      const T* uc = a.uc + rr;
+      for (i64 j = ws >> 1; j < (we >> 1); j++) {
+        T x = S(2 * j), y = S(2 * j + 1);
+        kaczmarz_pair(x, y, ldg(uc + j * ld), a.proj_diag);
+        S(2 * j) = x;
+        S(2 * j + 1) = y;
+      }
+    }
+    if (forward) {
+      T uL = ws > 0 ? S(ws - 1) : T(0);
+      T cur = S(ws);
+      for (i64 i = ws; i < we; i++) {
+        T nxt = (i + 1 < hi) ? S(i + 1) : T(0);
+        T v = gs_cell(a.gc, i, n, uL, cur, nxt, ldg(f + i * ld));
+        S(i) = v;
+        uL = v;
+        cur = nxt;
+      }
+    } else {
+      T uR = we < n ? S(we) : T(0);
+      T cur = S(we - 1);
+      for (i64 i = we - 1; i >= ws; i--) {
+        T prv = (i - 1 >= lo) ? S(i - 1) : T(0);
+        T v = gs_cell(a.gc, i, n, prv, cur, uR, ldg(f + i * ld));
+        S(i) = v;
+        uR = v;
+        cur = prv;
+      }
+    }
+    forward = !forward;
+  }
+  if (store) {
+    T* o = a.out + r;
+    for (i64 i = os; i < oe; i++) o[i * ld] = S(i);
+  }
+#undef S
+}
+
+template <typename T>
+void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s) {
+  require(d.n >= 2 && is_pow2(d.n), "smooth: level size must be a power of two >= 2");
+  require(d.B >= 1 && d.ld >= d.B, "smooth: need 1 <= B <= ld");
+  require(d.ns >= 1, "smooth: ns must be >= 1");
+  require(d.u_in && d.f && d.out && d.scratch, "smooth: null pointer");
+  ScratchArgs<T> a;
+  a.n = d.n;
+  a.ld = d.ld;
+  a.B = d.B;
+  a.nrg = (d.B + 31) / 32;
+  require(d.sld >= (i64)a.nrg * 32, "smooth: scratch stride too small");
+  a.sld = d.sld;
+  a.ns = d.ns;
+  a.gc = make_coef<T>(d.n, d.omega);
+  a.proj_diag = (T)d.proj_diag;
+  a.olo = d.olo;
+  a.ohi = d.ohi;
+  a.elo = d.elo;
+  a.ehi = d.ehi;
+  a.soff = d.soff;
+  a.u_in = d.u_in;
+  a.f = d.f;
+  a.uc = d.uc;
+  a.out = d.out;
+  a.scratch = d.scratch;
+  if (d.olo) {
+    require(d.soff != nullptr, "smooth: patch arrays need scratch offsets");
+    a.P = d.P;
+    a.W = a.b = 0;
+  } else {
+    require(d.W >= 1 && d.n % d.W == 0, "smooth: owned width must divide n");
+    a.W = d.W;
+    a.b = d.b;
+    a.P = d.n / d.W;
+  }
+  if (a.P == 0) return;
+  i64 blocks = (a.P * a.nrg + 3) / 4;
+  if (d.uc) smooth_scratch_kernel<T, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+  else smooth_scratch_kernel<T, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+  check_launch("smooth_scratch_kernel");
+}
+
+template void launch_visit<double>(const VisitDesc<double>&, cudaStream_t);
+template void launch_visit<float>(const VisitDesc<float>&, cudaStream_t);
+template void launch_smooth_scratch<double>(const ScratchDesc<double>&, cudaStream_t);
+template void launch_smooth_scratch<float>(const ScratchDesc<float>&, cudaStream_t);
+
+}  // namespace fmgsr

@@ -1,0 +1,136 @@
+"""Native solve plan: one FMG-FAS(-SR) pass per call, scheduled in C++ and
+replayed as a CUDA graph (``fmgsr_plan_*`` in include/fmgsr_cuda.h).
+
+The plan owns its per-level device workspace (allocated once), fuses each
+level visit of the reference driver (cycles.py:137-222) into one kernel where
+eligible, and captures the whole cycle on first use for each (forcing,
+solution) buffer pair.  ``FmgPlan.solve`` is what ``cycles.fmg_solve`` calls
+on its fast path and what ``bench.py`` times.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+
+GEOM_HALO, GEOM_GLOBAL, GEOM_PATCHES = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class PlanKey:
+    m0: int
+    m: int
+    n_sr: int
+    ns: int
+    geom_mode: int
+    P: int
+    b: int
+    B: int
+    dtype: torch.dtype
+    omega: float
+    fused: bool = True
+    use_graph: bool = True
+
+
+def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
+                    use_graph: bool = True) -> PlanKey:
+    """PlanKey of a ``cycles.SolverConfig`` for a batch of B right-hand sides."""
+    from .mesh import HaloMode
+
+    sm = cfg.smoother
+    if sm.n_patches is not None:
+        mode, P = GEOM_PATCHES, sm.n_patches
+        b = sm.buffer if sm.buffer is not None else (sm.halo_mode.halo or 0)
+    elif sm.halo_mode is HaloMode.GLOBAL:
+        mode, P, b = GEOM_GLOBAL, 1, 0
+    else:
+        mode, P = GEOM_HALO, 1
+        b = sm.buffer if sm.buffer is not None else sm.halo_mode.halo
+    return PlanKey(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns, mode, int(P), int(b),
+                   int(B), dtype, float(sm.omega), fused, use_graph)
+
+
+class FmgPlan:
+    def __init__(self, key: PlanKey):
+        N.require_cuda()
+        self.key = key
+        d = N.PlanDesc()
+        d.m0, d.m, d.n_sr, d.ns = key.m0, key.m, key.n_sr, key.ns
+        d.geom_mode = key.geom_mode
+        d.dtype = 0 if key.dtype == torch.float64 else 1
+        d.P, d.b, d.B, d.ld = key.P, key.b, key.B, key.B
+        d.omega = key.omega
+        d.fused = int(key.fused)
+        d.use_graph = int(key.use_graph)
+        h = C.c_void_p()
+        N.check(N.lib().fmgsr_plan_create(C.byref(d), C.byref(h)), "plan_create")
+        self._h = h
+        self.N = 2 ** key.m
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.lib().fmgsr_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _check_io(self, forcing: torch.Tensor, out: torch.Tensor) -> None:
+        k = self.key
+        for name, t in (("forcing", forcing), ("solution", out)):
+            if not t.is_cuda or t.dtype != k.dtype or tuple(t.shape) != (self.N, k.B) \
+                    or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {k.dtype} CUDA tensor of shape "
+                                 f"({self.N}, {k.B})")
+
+    def solve(self, forcing: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """One FMG pass for the (2**m, B) forcing; returns the (2**m, B) solution."""
+        if out is None:
+            out = torch.empty_like(forcing)
+        self._check_io(forcing, out)
+        N.check(N.lib().fmgsr_plan_solve(self._h, forcing.data_ptr(), out.data_ptr(),
+                                         N.stream_ptr()), "plan_solve")
+        return out
+
+    def solve_timed(self, forcing: torch.Tensor, out: torch.Tensor):
+        """Launch op by op with CUDA events per level visit; returns
+        [(kind, level, ms)] with kind in top/down/up/direct."""
+        self._check_io(forcing, out)
+        cap = 8192
+        ms = (C.c_float * cap)()
+        lvl = (C.c_int32 * cap)()
+        kind = (C.c_int32 * cap)()
+        nv = C.c_int64()
+        N.check(N.lib().fmgsr_plan_solve_timed(self._h, forcing.data_ptr(), out.data_ptr(),
+                                               N.stream_ptr(), ms, lvl, kind, cap,
+                                               C.byref(nv)), "plan_solve_timed")
+        names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade"}
+        return [(names[kind[i]], lvl[i], ms[i]) for i in range(min(nv.value, cap))]
+
+    def info(self) -> dict:
+        inf = N.PlanInfo()
+        N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")
+        return {
+            "workspace_bytes": inf.workspace_bytes,
+            "launches_per_solve": inf.launches_per_solve,
+            "visits_per_solve": inf.visits_per_solve,
+            "alg_bytes_per_solve": inf.alg_bytes_per_solve,
+            "finest_visit_alg_bytes": inf.finest_visit_alg_bytes,
+        }
+
+
+_cache: dict[PlanKey, FmgPlan] = {}
+
+
+def get_plan(key: PlanKey) -> FmgPlan:
+    p = _cache.get(key)
+    if p is None:
+        if len(_cache) >= 8:
+            _cache.pop(next(iter(_cache)))
+        p = _cache[key] = FmgPlan(key)
+    return p

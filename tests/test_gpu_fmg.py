@@ -1,0 +1,194 @@
+"""Whole FMG-FAS(-SR) solves on the GPU: golden vectors from the reference,
+the C oracle on batches, the reference's driver invariants
+(test_cycles.py), and the one-cycle O(h^2) accuracy criterion."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+GEOM = {0: "halo", 1: "global", 2: "patches"}
+
+
+def config_from_params(fm, params):
+    m0, m, n_sr, ns, kind, P, b = (int(x) for x in params)
+    if kind == 2:
+        sm = fm.SmootherConfig(ns=ns, n_patches=P, buffer=b)
+    elif kind == 1:
+        sm = fm.SmootherConfig(ns=ns, halo_mode=fm.HaloMode.GLOBAL)
+    else:
+        sm = fm.SmootherConfig(ns=ns, halo_mode=fm.HaloMode(str(b)))
+    return fm.SolverConfig(hierarchy=fm.build_hierarchy(m0, m), n_sr=n_sr, smoother=sm)
+
+
+@pytest.mark.parametrize("path", ["plan_fused", "plan_unfused", "operators"])
+def test_fmg_matches_golden(fm, golden, path):
+    for name in golden["fmg_cases"]:
+        p = str(name) + "/"
+        cfg = config_from_params(fm, golden[p + "params"])
+        forcing = golden[p + "forcing"]
+        if path == "operators":
+            got, _ = fm.fmg_solve(cfg, forcing, keep_state=True)
+        else:
+            got, _ = fm.fmg_solve(cfg, forcing, fused=(path == "plan_fused"))
+        assert np.array_equal(got, golden[p + "solution"]), (path, str(name))
+
+
+def oracle_cfg(oracle, cfg):
+    sm = cfg.smoother
+    if sm.n_patches is not None:
+        return oracle.make_cfg(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns,
+                               oracle.GEOM_PATCHES, sm.n_patches, sm.buffer)
+    if sm.halo_mode is fm_global(sm):
+        return oracle.make_cfg(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns,
+                               oracle.GEOM_GLOBAL, 1, 0)
+    return oracle.make_cfg(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns, oracle.GEOM_HALO,
+                           1, sm.halo_mode.halo)
+
+
+def fm_global(sm):
+    from paper_1207_6720_b200.mesh import HaloMode
+
+    return HaloMode.GLOBAL
+
+
+@pytest.mark.parametrize("m,P,b,n_sr,ns", [
+    (10, 4, 2, 1, 1),        # config 1 geometry
+    (12, 64, 4, 1, 1),       # config 2 geometry, reduced N
+    (12, 64, 4, 0, 1),
+    (12, 16, 1, 1, 1),       # config 5 cells, odd buffer
+    (12, 1024, 8, 1, 1),
+    (12, 256, 4, 2, 1),
+    (13, 4096, 8, 1, 1),     # config 4 geometry (W = 2 on every level)
+    (10, 16, 4, 1, 2),       # V(2,2)
+    (10, 8, 3, 0, 2),
+])
+def test_fmg_batch_matches_oracle(fm, oracle, m, P, b, n_sr, ns):
+    B = 40
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + P + b))
+    got = fm.fmg_solve(cfg, f)[0].cpu().numpy()
+    got_unfused = fm.fmg_solve(cfg, f, fused=False)[0].cpu().numpy()
+    want = oracle.fmg_solve_batch(oracle_cfg(oracle, cfg), np.ascontiguousarray(f.cpu().numpy().T),
+                                  nthreads=8).T
+    assert np.array_equal(got, want)
+    assert np.array_equal(got_unfused, want)
+
+
+def test_zero_forcing_gives_zero(fm):
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 5), n_sr=1,
+                          smoother=fm.SmootherConfig(halo_mode=fm.HaloMode.HALO2))
+    sol, _ = fm.fmg_solve(cfg, np.zeros(32))
+    assert not np.any(sol)
+
+
+def test_rejects_bad_config_and_size(fm):
+    with pytest.raises(ValueError):
+        fm.SolverConfig(hierarchy=fm.build_hierarchy(1, 6))
+    with pytest.raises(ValueError):
+        fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 6), n_sr=4)
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 5))
+    with pytest.raises(ValueError):
+        fm.fmg_solve(cfg, np.zeros(16))
+
+
+@pytest.mark.parametrize("mode,ns,n_sr", [
+    (("halo", 2), 1, 2), (("halo", 4), 2, 1), (("global", 0), 1, 3), (("patches", 8), 1, 2)])
+def test_expand_sr_reproduces_finest_field(fm, mode, ns, n_sr):
+    if mode[0] == "patches":
+        sm = fm.SmootherConfig(ns=ns, n_patches=mode[1], buffer=3)
+    elif mode[0] == "global":
+        sm = fm.SmootherConfig(ns=ns, halo_mode=fm.HaloMode.GLOBAL)
+    else:
+        sm = fm.SmootherConfig(ns=ns, halo_mode=fm.HaloMode(str(mode[1])))
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 6), n_sr=n_sr, smoother=sm)
+    forcing = fm.manufactured_rhs(64)
+    solution, diag = fm.fmg_solve(cfg, forcing, keep_state=True)
+    rebuilt = fm.expand_sr(diag.state, cfg)
+    assert np.array_equal(rebuilt[:, 0].cpu().numpy(), solution)
+    # and the fast path (native plan) gives the same field
+    fast, _ = fm.fmg_solve(cfg, forcing)
+    assert np.array_equal(fast, solution)
+
+
+@pytest.mark.parametrize("mode", [fm_mode for fm_mode in ("2", "4")])
+def test_debug_sr_poisoning_changes_nothing(fm, mode):
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 6), n_sr=2,
+                          smoother=fm.SmootherConfig(halo_mode=fm.HaloMode(mode)))
+    forcing = fm.manufactured_rhs(64)
+    plain, _ = fm.fmg_solve(cfg, forcing)
+    poisoned, _ = fm.fmg_solve(cfg, forcing, debug_sr=True)
+    assert np.all(np.isfinite(poisoned))
+    assert np.array_equal(plain, poisoned)
+
+
+def test_final_working_rhs_is_original(fm):
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 5), n_sr=1,
+                          smoother=fm.SmootherConfig(halo_mode=fm.HaloMode.HALO2))
+    forcing = fm.manufactured_rhs(32)
+    _, diag = fm.fmg_solve(cfg, forcing, keep_state=True)
+    st = diag.state
+    assert torch.equal(st.f_work[5], st.f_orig[5])
+    assert np.array_equal(st.f_orig[5][:, 0].cpu().numpy(), forcing)
+    assert np.array_equal(st.f_orig[4][:, 0].cpu().numpy(), fm.restrict(forcing))
+
+
+@pytest.mark.parametrize("mode", ["2", "4", "global"])
+def test_cycle_contracts_algebraic_error(fm, mode):
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(2, 7),
+                          smoother=fm.SmootherConfig(halo_mode=fm.HaloMode(mode)))
+    _, diag = fm.fmg_solve(cfg, fm.manufactured_rhs(128), collect_diagnostics=True)
+    assert len(diag.levels) == 5
+    for lev in diag.levels:
+        assert lev.error_after_cycle < lev.error_after_prolong
+        assert lev.gamma < 0.5
+        assert np.isfinite(lev.residual_after_cycle)
+
+
+def test_config1_truncation_accuracy(fm):
+    """BASELINE config 1: N=2^10, m0=3, 4 SR patches, b=2, V(1,1), n_sr=1:
+    one FMG cycle reaches the discretisation error (<= 2x direct solve)."""
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, 10), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=4, buffer=2))
+    f, uex = fm.sine_problem(1024)
+    sol, _ = fm.fmg_solve(cfg, f)
+    direct = fm.direct_fine_solve(f)
+    e_fmg = fm.rel_l2_error(sol, uex)
+    e_dir = fm.rel_l2_error(direct, uex)
+    assert e_fmg <= 2.0 * e_dir
+
+
+@pytest.mark.slow
+def test_config2_full_size(fm, oracle):
+    """BASELINE config 2 at full size: N=2^16, P=64, b=4, B=1024, n_sr=1.
+    Bitwise against the oracle on 8 seeded RHS; O(h^2) criterion on all."""
+    m, B = 16, 1024
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=64, buffer=4))
+    coef = fm.fourier_coefficients(B, seed=0)
+    f, uex = fm.fourier_batch(2 ** m, coef)
+    sol, _ = fm.fmg_solve(cfg, f)
+    cols = [0, 1, 63, 64, 255, 511, 777, 1023]
+    fh = f[:, cols].cpu().numpy().T.copy()
+    want = oracle.fmg_solve_batch(oracle_cfg(oracle, cfg), fh, nthreads=8).T
+    assert np.array_equal(sol[:, cols].cpu().numpy(), want)
+    direct = fm.direct_fine_solve(f)
+    err = torch.linalg.vector_norm(sol - uex, dim=0) / torch.linalg.vector_norm(uex, dim=0)
+    derr = torch.linalg.vector_norm(direct - uex, dim=0) / torch.linalg.vector_norm(uex, dim=0)
+    assert bool((err <= 2.0 * derr).all())
+
+
+def test_float32_variant_bound(fm):
+    """fp32 variant against the fp64 result: per-RHS inf-relative gap within the
+    stated bound (2e-3 at N=2^12, growing ~ N)."""
+    m, B = 12, 32
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=64, buffer=4))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=9))
+    s64 = fm.fmg_solve(cfg, f)[0]
+    s32 = fm.fmg_solve(cfg, f.float())[0]
+    assert s32.dtype == torch.float32
+    gap = (s32.double() - s64).abs().amax(0) / s64.abs().amax(0)
+    assert float(gap.max()) <= 2e-3
