@@ -1,0 +1,346 @@
+"""Benchmark of one FMG-FAS-SR cycle (BASELINE.json metric: fine-grid
+unknowns solved per second for one cycle, and % of the HBM roofline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload config2]
+    python bench.py --impl reference ...      # the CPU reference path (oracle port)
+
+A step is one ``fmg_solve`` of a batch of B right-hand sides (one FMG pass:
+one V-cycle per level) through the native plan (CUDA graph of fused level
+visits).  Under torchrun every rank solves its own batch of B independent
+right-hand sides (independent objects, no data-path collective, weak
+scaling); the time is the max over ranks.  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: the metric's configuration (fits one GPU)
+    "config2": dict(m0=3, m=16, P=64, b=4, ns=1, n_sr=1, B=1024, dtype="f64"),
+    "config1": dict(m0=3, m=10, P=4, b=2, ns=1, n_sr=1, B=1, dtype="f64"),
+    "config4": dict(m0=3, m=24, P=4096, b=8, ns=1, n_sr=1, B=64, dtype="f64"),
+    "config5": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f64"),
+    "config5_f32": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f32"),
+}
+METRIC = "fine-grid unknowns solved/sec (one FMG-FAS-SR cycle)"
+UNIT = "unknowns/s"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------
+# CPU reference path: the oracle port (C restatement of the reference algorithm)
+# ---------------------------------------------------------------------------------------
+def cpu_rate(w, budget_s: float, nthreads: int, seed: int = 1):
+    """Solve a bounded sample of the workload's RHS on the host; returns
+    (unknowns/s, n_rhs, seconds).  Test infrastructure: oracle/liboracle.so."""
+    from oracle import oracle as O
+
+    n = 2 ** w["m"]
+    cfg = O.make_cfg(w["m0"], w["m"], w["n_sr"], w["ns"], O.GEOM_PATCHES, w["P"], w["b"])
+    x = (np.arange(n) + 0.5) / n
+
+    def rhs(k):
+        # 4 distinct seeded Fourier rows, tiled (the solve time does not depend on values)
+        base = np.zeros((4, n))
+        a = np.random.default_rng(seed).standard_normal((4, 32)) / np.arange(1, 33) ** 2
+        for j in range(1, 33):
+            base += a[:, j - 1:j] * np.sin(j * np.pi * x)[None, :]
+        return np.ascontiguousarray(np.tile(base, (k // 4 + 1, 1))[:k])
+
+    t0 = time.perf_counter()
+    O.fmg_solve_batch(cfg, rhs(1), 1)  # calibrate on one RHS, one thread
+    t1 = time.perf_counter() - t0
+    k = max(nthreads, int(budget_s * nthreads / max(t1, 1e-6)))
+    k = min(k, w["B"] * 64)
+    f = rhs(k)
+    t0 = time.perf_counter()
+    O.fmg_solve_batch(cfg, f, nthreads)
+    dt = time.perf_counter() - t0
+    return k * n / dt, k, dt
+
+
+def run_reference(args, w):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    nthreads = os.cpu_count() or 1
+    n = 2 ** w["m"]
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        v, k, dt = cpu_rate(w, args.ref_step_s, nthreads, seed=i)
+        if i >= args.warmup:
+            vals.append((v, k, dt))
+        sample = f"{k} seeded RHS of N={n} (P={w['P']}, b={w['b']}) per step, {dt:.1f} s"
+    tot_unk = sum(v[1] for v in vals) * n
+    tot_t = sum(v[2] for v in vals)
+    value = tot_unk / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / len(vals), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+        "config": workload_config(args.workload, w, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name, w, world):
+    return {
+        "workload": f"{name}: 1D Poisson FMG-FAS-SR, N=2^{w['m']} fine cells, m0={w['m0']}, "
+                    f"{w['P']} patches, {w['b']}-cell buffer, V({w['ns']},{w['ns']}), "
+                    f"n_sr={w['n_sr']}, batch {w['B']} seeded Fourier RHS per GPU",
+        "N": 2 ** w["m"], "batch_per_gpu": w["B"], "global_batch": w["B"] * world,
+        "patches": w["P"], "buffer": w["b"], "ns": w["ns"], "n_sr": w["n_sr"], "m0": w["m0"],
+        "parallelism": f"dp{world} (independent RHS batches per GPU)",
+        "l2": "inputs larger than L2: every field of the finest level is "
+              f"{2 ** w['m'] * w['B'] * (8 if w['dtype'] == 'f64' else 4) / 2**20:.0f} MiB; no flush",
+    }
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------------------
+# GPU path
+# ---------------------------------------------------------------------------------------
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(workload)
+    except Exception:
+        return None
+
+
+def run_gpu(args, w):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1207_6720_b200 as fm
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = torch.float64 if w["dtype"] == "f64" else torch.float32
+    m, B = w["m"], w["B"]
+    n = 2 ** m
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], m), n_sr=w["n_sr"],
+                          smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+    plan = fm.get_plan(fm.key_from_config(cfg, B, dtype))
+    coef = fm.fourier_coefficients(B, seed=1000 * rank)
+    f, _ = fm.fourier_batch(n, coef, dtype, with_exact=False)
+    sol = torch.empty_like(f)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        plan.solve(f, sol)
+    torch.cuda.synchronize()
+    info = plan.info()
+
+    # ---- device-resident throughput (value) --------------------------------------
+    clk = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.solve(f, sol)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * B * n / (ms_step / 1e3)
+
+    # ---- end to end through the public API with host buffers ----------------------
+    hf = f.cpu().pin_memory()
+    hs = torch.empty_like(hf).pin_memory()
+    dfi = torch.empty_like(f)
+    dso = torch.empty_like(f)
+
+    def e2e_step():
+        dfi.copy_(hf, non_blocking=True)
+        plan.solve(dfi, dso)
+        hs.copy_(dso, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item()) / args.steps
+    e2e_val = world * B * n / (e2e_ms / 1e3)
+    nbytes = n * B * (8 if dtype == torch.float64 else 4)
+
+    # ---- per-visit kernel times (CUDA events on the launching stream) -------------
+    visits = []
+    for _ in range(max(1, min(args.steps, 5))):
+        visits += plan.solve_timed(f, sol)
+    finest = [(k, ms_) for (k, lvl, ms_) in visits if lvl == m and k in ("top", "up")]
+    by_level = {}
+    for (k, lvl, ms_) in visits:
+        by_level[lvl] = by_level.get(lvl, 0.0) + ms_
+    tot = sum(by_level.values())
+    esz = 8 if dtype == torch.float64 else 4
+    # algorithmic words per cell of the finest visits: T_m and U_m
+    sr_m = cfg.is_sr_level(m)
+    words = {"top": 2.5 + (0.0 if sr_m else 1.0), "up": 2.5 + (0.0 if sr_m else 1.0)}
+    alg = sum(words[k] * n * B * esz for k, _ in finest)
+    dur = sum(ms_ for _, ms_ in finest) / 1e3
+    achieved = alg / dur / 1e9 if dur > 0 else None
+    peak, peak_src = measured_peak()
+    share = sum(ms_ for _, ms_ in finest) / tot if tot else None
+    traffic = committed_traffic(args.workload)
+    whole_alg = info["alg_bytes_per_solve"]
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, k, dt = cpu_rate(w, args.cpu_budget_s, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": f"{k} seeded RHS of N={n} (P={w['P']}, b={w['b']}) on "
+                             f"{os.cpu_count()} host threads, {dt:.1f} s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": w["dtype"], "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
+            "config": workload_config(args.workload, w, world),
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None,
+                "traffic": traffic,
+                "kernel": "visit_kernel at the finest level (T_m: FMG prolongation + "
+                          "patch GS + restriction/tau; U_m: FMG prolongation + Kaczmarz CR + "
+                          "patch GS)",
+                "alg_bytes_per_launch": alg / max(1, len(finest)),
+                "launches_measured": len(finest),
+                "share_of_step": share, "peak_source": peak_src,
+                "whole_cycle_alg_bytes": whole_alg,
+                "whole_cycle_frac": whole_alg / (ms_step / 1e3) / 1e9 / peak,
+            },
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms},
+            "gpu_launches": info["launches_per_solve"] * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+    return run_gpu(args, w)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -3,86 +3,167 @@
 // One lane runs the Gauss-Seidel chain of one (patch, rhs): the reference's
 // per-patch solve (_kernels_numba.py:79-91) with ns = 1.  Because a single
 // forward sweep never lets a cell right of the owned range influence an owned
-// cell, the chain stops at the owned end oe (cells [oe, we) are computed and
-// discarded by the reference; the cell oe itself is read as frozen data).
-// Input pairs come from a PairSource (plain load, FAS correction, or FMG
-// prolongation, each with optional just-in-time Kaczmarz), raw loads are
-// prefetched PF pairs ahead in registers, and owned results are stored and/or
-// pushed into the restriction/tau epilogue.
+// cell, the chain stops at the owned end oe (the reference computes cells
+// [oe, we) and discards them; the cell oe itself is read as frozen data).
+//
+// Input rows are staged D-1 pairs ahead by cp.async into a per-lane ring in
+// shared memory (no prefetch registers, one async group per pair).  Pairs
+// that touch anything special -- the frozen cell left of the window, domain
+// boundary rows, FMG boundary rows, the Kaczmarz window ends, the first two
+// owned pairs of the restriction epilogue, clamped loads near the last row --
+// go through step_slow(), which evaluates every case like the reference.
+// The remaining interior pairs run in fast loops with no per-cell branches
+// and pointer-walking addresses.
 #pragma once
 
 #include "fmgsr_device.cuh"
 
 namespace fmgsr {
 
-#ifndef FMGSR_PF
-#define FMGSR_PF 4
-#endif
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D>
+struct Chain {
+  static constexpr int R = SrcRows<SRC, CR>::R;
+  PairSource<T, SRC, CR> src;
+  GsCoef<T> gc;
+  i64 n, nc, ld, ws, os, oe;
+  T* out;  // u_l output, column-offset (nullptr: not written)
+  bool store;
+  T* ring;  // this lane's ring: slot s, row k at ring[(s * R + k) * NT]
+  Epilogue<T>* epi;
+  // chain state: uL = new value left of the current pair; (v0, v1, f0, f1) = current pair
+  T uL, v0, v1, f0, f1;
 
-template <typename T, int SRC, bool CR, bool EPI>
-__device__ __forceinline__ void run_chain_ns1(PairSource<T, SRC, CR>& src, const GsCoef<T>& gc,
-                                              i64 n, i64 ws, i64 os, i64 oe, T* out, i64 ld,
-                                              bool write_u, bool store, Epilogue<T>* epi) {
-  constexpr int PF = FMGSR_PF;
-  const i64 e = oe;  // cells [ws, e) are updated
-  const i64 qs = (ws > 0) ? ((ws - 1) >> 1) : 0;
-  const i64 qe = (e - 1) >> 1;
+  __device__ __forceinline__ T* slot(i64 x) const { return ring + (i64)((x & (D - 1)) * R) * NT; }
 
-  src.init(qs);
-  T v0, v1, f0, f1;
-  {
-    Raw<T> r = src.load(qs);
-    src.make(qs, r, v0, v1);
+  __device__ __forceinline__ T gsi(T l, T u, T r, T f) const {
+    T s = xsub(xsub(xmul(T(2), u), l), r);
+    T resid = xsub(f, xmul(gc.inv_h2, s));
+    if (!OMEGA1) resid = xmul(gc.omega, resid);  // omega == 1: the product is exact
+    return xadd(u, xmul(resid, gc.rdiag));
+  }
+
+  // general step for pair q (every boundary case, exactly as the reference)
+  __device__ __forceinline__ void step_slow(i64 q) {
+    cp_wait<D - 2>();
+    Raw<T> r = src.template fetch<NT>(slot(q + 1));
+    src.template issue<NT>(slot(q), q + D);
+    cp_commit();
+    T w0, w1;
+    src.make(q + 1, r, w0, w1);
+    const i64 i0 = 2 * q, i1 = i0 + 1;
+    T n0 = v0, n1 = v1;
+    if (i0 < ws) {
+      uL = v0;  // frozen neighbour of the window
+    } else {
+      n0 = gs_cell(gc, i0, n, uL, v0, v1, f0);
+      uL = n0;
+    }
+    if (i1 < ws) {
+      uL = v1;
+    } else if (i1 < oe) {
+      n1 = gs_cell(gc, i1, n, uL, v1, w0, f1);
+      uL = n1;
+    }
+    if (EPI) {
+      if (i0 >= os) {  // owned pairs are whole pairs (os, oe even)
+        if (out && store) {
+          out[i0 * ld] = n0;
+          out[i1 * ld] = n1;
+        }
+        epi->push(q, n0, n1, f0, f1, store);
+      }
+    } else if (store) {
+      if (i0 >= os && i0 < oe) out[i0 * ld] = n0;
+      if (i1 >= os && i1 < oe) out[i1 * ld] = n1;
+    }
+    v0 = w0;
+    v1 = w1;
     f0 = r.f0;
     f1 = r.f1;
   }
-  Raw<T> ring[PF];
-#pragma unroll
-  for (int k = 0; k < PF; k++) ring[k] = src.load(qs + 1 + k);
 
-  T uL = T(0);
-  for (i64 q = qs; q <= qe; q += PF) {
-#pragma unroll
-    for (int k = 0; k < PF; k++) {
-      const i64 qq = q + k;
-      if (qq <= qe) {
-        T w0, w1;
-        src.make(qq + 1, ring[k], w0, w1);
-        const T g0 = ring[k].f0, g1 = ring[k].f1;
-        ring[k] = src.load(qq + 1 + PF);
-        const i64 i0 = 2 * qq, i1 = i0 + 1;
-        T n0 = v0, n1 = v1;
-        if (i0 < ws) {
-          uL = v0;  // frozen neighbour of the window
-        } else {
-          n0 = gs_cell(gc, i0, n, uL, v0, v1, f0);
-          uL = n0;
+  // interior pairs [q, q_end]: OWNED selects store/epilogue
+  template <bool OWNED>
+  __device__ __forceinline__ void run_fast(i64 q, i64 q_end) {
+    src.fast_ptrs(q + D);
+    T* po = (OWNED && out) ? out + (2 * q) * ld : nullptr;
+    if (EPI && OWNED) epi->fast_begin(q);
+    const bool st_u = OWNED && out && store;
+#pragma unroll 2
+    for (; q <= q_end; q++) {
+      cp_wait<D - 2>();
+      Raw<T> r = src.template fetch<NT>(slot(q + 1));
+      src.template issue_fast<NT>(slot(q));
+      cp_commit();
+      T w0, w1;
+      src.make_fast(r, w0, w1);
+      T n0 = gsi(uL, v0, v1, f0);
+      T n1 = gsi(n0, v1, w0, f1);
+      uL = n1;
+      if (OWNED) {
+        if (st_u) {
+          po[0] = n0;
+          po[ld] = n1;
         }
-        if (i1 < ws) {
-          uL = v1;
-        } else if (i1 < e) {
-          n1 = gs_cell(gc, i1, n, uL, v1, w0, f1);
-          uL = n1;
-        }
-        if (EPI) {
-          if (i0 >= os) {  // owned pairs are whole pairs (os, oe even)
-            if (write_u && store) {
-              out[i0 * ld] = n0;
-              out[i1 * ld] = n1;
-            }
-            epi->push(qq, n0, n1, f0, f1, store);
-          }
-        } else if (store) {
-          if (i0 >= os && i0 < oe) out[i0 * ld] = n0;
-          if (i1 >= os && i1 < oe) out[i1 * ld] = n1;
-        }
-        v0 = w0;
-        v1 = w1;
-        f0 = g0;
-        f1 = g1;
+        if (po) po += 2 * ld;
+        if (EPI) epi->push_fast(n0, n1, f0, f1, store);
       }
+      v0 = w0;
+      v1 = w1;
+      f0 = r.f0;
+      f1 = r.f1;
     }
   }
-}
+
+  __device__ __forceinline__ void run(i64 we) {
+    const i64 qs = (ws > 0) ? ((ws - 1) >> 1) : 0;
+    const i64 qe = (oe - 1) >> 1;
+    // chain head: state before pair qs, pair qs itself, then D-1 staged pairs
+    src.init(qs);
+    {
+      Raw<T> r = src.load(qs);
+      src.make(qs, r, v0, v1);
+      f0 = r.f0;
+      f1 = r.f1;
+    }
+    for (int k = 1; k < D; k++) {
+      src.template issue<NT>(slot(qs + k), qs + k);
+      cp_commit();
+    }
+    uL = T(0);
+    // interior range: both cells updated and interior, generation of q+1
+    // interior, CR window interior, unclamped fast issue of q + D
+    i64 lo = (ws + 1) >> 1;
+    if (lo < 1) lo = 1;
+    i64 hi = (oe - 2) >> 1;
+    if (hi > nc - 2) hi = nc - 2;
+    if (SRC == SRC_FMG) hi = hi < nc - 4 ? hi : nc - 4;
+    if (SRC == SRC_CORR) hi = hi < nc - 3 ? hi : nc - 3;
+    if (CR) {
+      const i64 a = src.wlo - 1, b = (we >> 1) - 2;
+      lo = lo > a ? lo : a;
+      hi = hi < b ? hi : b;
+    }
+    hi = hi < nc - 3 - D ? hi : nc - 3 - D;
+    const i64 oq = os >> 1;
+    i64 q = qs;
+    // buffer cells left of the owned range
+    const i64 bl = lo, bh = hi < oq - 1 ? hi : oq - 1;
+    if (bl <= bh) {
+      for (; q < bl; q++) step_slow(q);
+      run_fast<false>(q, bh);
+      q = bh + 1;
+    }
+    // owned cells
+    const i64 ol = lo > oq + (EPI ? 2 : 0) ? lo : oq + (EPI ? 2 : 0);
+    if (ol <= hi) {
+      for (; q < ol; q++) step_slow(q);
+      run_fast<true>(q, hi);
+      q = hi + 1;
+    }
+    for (; q <= qe; q++) step_slow(q);
+    cp_wait<0>();
+  }
+};
 
 }  // namespace fmgsr

@@ -75,13 +75,36 @@ __device__ __forceinline__ T gs_cell(const GsCoef<T>& c, i64 i, i64 n, T uL, T u
 
 // Kaczmarz projection of one pair onto its coarse value, reference
 // _kernels_numba.py:53-56: r = uc - 0.5(a+b); t = r/proj_diag; a,b += 0.5 t.
+// When proj_diag is a power of two (the reference's 0.5) the division is an
+// exact multiply by its reciprocal.
 template <typename T>
-__device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, T proj_diag) {
+struct KzCoef {
+  T proj_diag, recip;
+  bool pow2;
+};
+
+template <typename T>
+__device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, const KzCoef<T>& k) {
   T r = xsub(uc, xmul(T(0.5), xadd(a, b)));
-  T t = xdiv(r, proj_diag);
+  T t = k.pow2 ? xmul(r, k.recip) : xdiv(r, k.proj_diag);
   T h = xmul(T(0.5), t);
   a = xadd(a, h);
   b = xadd(b, h);
+}
+
+// cp.async (LDGSTS) staging: each lane copies exactly the elements it will
+// consume into its own shared-memory column, so a lane only ever waits on
+// its own async groups (no warp or block synchronisation in the pipeline).
+template <typename T>
+__device__ __forceinline__ void cp_async(T* smem, const T* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(sizeof(T))
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -94,8 +117,9 @@ __device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, T proj_diag) {
 // With CR the pair is projected (Kaczmarz) when it lies in the patch's pair
 // range [ws//2, we//2): exactly the pairs the reference kaczmarz_sweep visits
 // before the GS pass (_kernels_numba.py:42-57, 87-89), applied just in time.
-// Loads are split (load(): raw global reads, no dependencies) from make()
-// (arithmetic + sliding window) so the caller can prefetch raws ahead.
+// The raw rows of a pair are staged by cp.async into a per-lane ring slot
+// (issue*), read back with fetch(), and turned into values by make*():
+// make() handles every boundary row, make_fast() the interior only.
 // ---------------------------------------------------------------------------
 enum { SRC_LOAD = 0, SRC_CORR = 1, SRC_FMG = 2 };
 
@@ -104,39 +128,126 @@ struct Raw {
   T a0, a1, h, g, f0, f1;
 };
 
+template <int SRC, bool CR>
+struct SrcRows {
+  // staged rows per pair: f(2) + LOAD u(2) | CORR u(2)+uH(1) | FMG uH(1), + uc(1) with CR
+  static constexpr int R =
+      2 + (SRC == SRC_LOAD ? 2 : SRC == SRC_CORR ? 3 : 1) + ((CR && SRC != SRC_FMG) ? 1 : 0);
+};
+
 template <typename T, int SRC, bool CR>
 struct PairSource {
+  static constexpr int R = SrcRows<SRC, CR>::R;
   const T* u;   // fine field, column-offset (LOAD, CORR)
   const T* uH;  // coarse field (CORR, FMG; CR target for FMG)
   const T* uc;  // CR target for LOAD / CORR
   const T* f;   // level right-hand side
   i64 ld, nc;   // row stride, number of pairs (= coarse cells)
-  T proj_diag;
+  KzCoef<T> kz;
   i64 wlo, whi;  // Kaczmarz pair range
   T s0, s1, s2, s3;
+  // fast-issue row pointers (pair g): f row 2g, u row (LOAD 2g | CORR 2g+2),
+  // uH row (CORR g+1 | FMG g+2), uc row g
+  const T *pf, *pu, *ph, *pc;
 
   __device__ __forceinline__ i64 cl(i64 q) const { return q < 0 ? 0 : (q >= nc ? nc - 1 : q); }
 
+  // slot layout: sl[k * NT] for k < R (NT = threads per block)
+  template <int NT>
+  __device__ __forceinline__ void issue(T* sl, i64 g) const {
+    i64 gg = cl(g);
+    cp_async(sl, f + (2 * gg) * ld);
+    cp_async(sl + NT, f + (2 * gg + 1) * ld);
+    if (SRC == SRC_LOAD) {
+      cp_async(sl + 2 * NT, u + (2 * gg) * ld);
+      cp_async(sl + 3 * NT, u + (2 * gg + 1) * ld);
+    } else if (SRC == SRC_CORR) {
+      i64 g1 = cl(g + 1);
+      cp_async(sl + 2 * NT, u + (2 * g1) * ld);
+      cp_async(sl + 3 * NT, u + (2 * g1 + 1) * ld);
+      cp_async(sl + 4 * NT, uH + g1 * ld);
+    } else {
+      cp_async(sl + 2 * NT, uH + cl(g + 2) * ld);
+    }
+    if (CR && SRC != SRC_FMG) cp_async(sl + (R - 1) * NT, uc + gg * ld);
+  }
+
+  __device__ __forceinline__ void fast_ptrs(i64 g) {
+    pf = f + (2 * g) * ld;
+    if (SRC == SRC_LOAD) pu = u + (2 * g) * ld;
+    if (SRC == SRC_CORR) {
+      pu = u + (2 * g + 2) * ld;
+      ph = uH + (g + 1) * ld;
+    }
+    if (SRC == SRC_FMG) ph = uH + (g + 2) * ld;
+    if (CR && SRC != SRC_FMG) pc = uc + g * ld;
+  }
+
+  // unclamped issue of the pair at the fast pointers, then advance one pair
+  template <int NT>
+  __device__ __forceinline__ void issue_fast(T* sl) {
+    cp_async(sl, pf);
+    cp_async(sl + NT, pf + ld);
+    pf += 2 * ld;
+    if (SRC == SRC_LOAD) {
+      cp_async(sl + 2 * NT, pu);
+      cp_async(sl + 3 * NT, pu + ld);
+      pu += 2 * ld;
+    } else if (SRC == SRC_CORR) {
+      cp_async(sl + 2 * NT, pu);
+      cp_async(sl + 3 * NT, pu + ld);
+      cp_async(sl + 4 * NT, ph);
+      pu += 2 * ld;
+      ph += ld;
+    } else {
+      cp_async(sl + 2 * NT, ph);
+      ph += ld;
+    }
+    if (CR && SRC != SRC_FMG) {
+      cp_async(sl + (R - 1) * NT, pc);
+      pc += ld;
+    }
+  }
+
+  template <int NT>
+  __device__ __forceinline__ Raw<T> fetch(const T* sl) const {
+    Raw<T> r;
+    r.f0 = sl[0];
+    r.f1 = sl[NT];
+    r.a0 = r.a1 = r.h = r.g = T(0);
+    if (SRC == SRC_LOAD) {
+      r.a0 = sl[2 * NT];
+      r.a1 = sl[3 * NT];
+    } else if (SRC == SRC_CORR) {
+      r.a0 = sl[2 * NT];
+      r.a1 = sl[3 * NT];
+      r.h = sl[4 * NT];
+    } else {
+      r.h = sl[2 * NT];
+    }
+    if (CR && SRC != SRC_FMG) r.g = sl[(R - 1) * NT];
+    return r;
+  }
+
+  // direct (uncached-path) load of a pair, for the chain head
   __device__ __forceinline__ Raw<T> load(i64 q) const {
     Raw<T> r;
     i64 qq = cl(q);
-    r.f0 = ldg(f + (2 * qq) * ld);
-    r.f1 = ldg(f + (2 * qq + 1) * ld);
+    r.f0 = f[(2 * qq) * ld];
+    r.f1 = f[(2 * qq + 1) * ld];
+    r.a0 = r.a1 = r.h = r.g = T(0);
     if (SRC == SRC_LOAD) {
-      r.a0 = ldg(u + (2 * qq) * ld);
-      r.a1 = ldg(u + (2 * qq + 1) * ld);
-      r.h = T(0);
+      r.a0 = u[(2 * qq) * ld];
+      r.a1 = u[(2 * qq + 1) * ld];
     } else if (SRC == SRC_CORR) {
       i64 q1 = cl(q + 1);
-      r.a0 = ldg(u + (2 * q1) * ld);
-      r.a1 = ldg(u + (2 * q1 + 1) * ld);
-      r.h = ldg(uH + q1 * ld);
+      r.a0 = u[(2 * q1) * ld];
+      r.a1 = u[(2 * q1 + 1) * ld];
+      r.h = uH[q1 * ld];
     } else {
-      r.a0 = r.a1 = T(0);
-      r.h = ldg(uH + cl(q + 2) * ld);
+      r.h = uH[cl(q + 2) * ld];
     }
-    if (CR && SRC != SRC_FMG) r.g = ldg(uc + qq * ld);
-    else r.g = T(0);
+    if (CR && SRC != SRC_FMG) r.g = uc[qq * ld];
     return r;
   }
 
@@ -144,22 +255,28 @@ struct PairSource {
   __device__ __forceinline__ void init(i64 q) {
     if (SRC == SRC_CORR) {
       // s0 = c_{q-1}, s1 = c_q, s2 = u[2q], s3 = u[2q+1]; c_j = uH[j] - 0.5(u[2j] + u[2j+1])
-      s2 = ldg(u + (2 * q) * ld);
-      s3 = ldg(u + (2 * q + 1) * ld);
-      s1 = xsub(ldg(uH + q * ld), xmul(T(0.5), xadd(s2, s3)));
+      s2 = u[(2 * q) * ld];
+      s3 = u[(2 * q + 1) * ld];
+      s1 = xsub(uH[q * ld], xmul(T(0.5), xadd(s2, s3)));
       if (q >= 1) {
-        T a = ldg(u + (2 * q - 2) * ld), b = ldg(u + (2 * q - 1) * ld);
-        s0 = xsub(ldg(uH + (q - 1) * ld), xmul(T(0.5), xadd(a, b)));
+        T a = u[(2 * q - 2) * ld], b = u[(2 * q - 1) * ld];
+        s0 = xsub(uH[(q - 1) * ld], xmul(T(0.5), xadd(a, b)));
       } else {
         s0 = T(0);
       }
     } else if (SRC == SRC_FMG) {
       // s0..s3 = c[q-2], c[q-1], c[q], c[q+1] (clamped; boundary rows ignore them)
-      s0 = ldg(uH + cl(q - 2) * ld);
-      s1 = ldg(uH + cl(q - 1) * ld);
-      s2 = ldg(uH + cl(q) * ld);
-      s3 = ldg(uH + cl(q + 1) * ld);
+      s0 = uH[cl(q - 2) * ld];
+      s1 = uH[cl(q - 1) * ld];
+      s2 = uH[cl(q) * ld];
+      s3 = uH[cl(q + 1) * ld];
     }
+  }
+
+  // interior FMG rows (stencils.py:90-97), then /128 as an exact scaling
+  __device__ __forceinline__ void fmg_interior(T c4, T& e, T& o) const {
+    e = xsub(xadd(xadd(xmul(T(-5), s0), xmul(T(35), s1)), xmul(T(105), s2)), xmul(T(7), s3));
+    o = xsub(xadd(xadd(xmul(T(-7), s1), xmul(T(105), s2)), xmul(T(35), s3)), xmul(T(5), c4));
   }
 
   __device__ __forceinline__ void make(i64 q, const Raw<T>& r, T& v0, T& v1) {
@@ -182,8 +299,7 @@ struct PairSource {
       const T c0 = s0, c1 = s1, c2 = s2, c3 = s3, c4 = r.h;  // c[q-2 .. q+2]
       T e, o;
       if (q >= 2 && q <= nc - 3) {
-        e = xsub(xadd(xadd(xmul(T(-5), c0), xmul(T(35), c1)), xmul(T(105), c2)), xmul(T(7), c3));
-        o = xsub(xadd(xadd(xmul(T(-7), c1), xmul(T(105), c2)), xmul(T(35), c3)), xmul(T(5), c4));
+        fmg_interior(c4, e, o);
       } else if (q == 0) {  // rows 0, 1 over c[0..2] = c2, c3, c4
         e = xsub(xmul(T(70), c2), xmul(T(2), c3));
         o = xsub(xadd(xmul(T(112), c2), xmul(T(35), c3)), xmul(T(5), c4));
@@ -197,15 +313,43 @@ struct PairSource {
         e = xsub(xadd(xmul(T(112), c2), xmul(T(35), c1)), xmul(T(5), c0));
         o = xsub(xmul(T(70), c2), xmul(T(2), c1));
       }
-      v0 = xdiv(e, T(128));
-      v1 = xdiv(o, T(128));
+      v0 = xmul(e, T(0.0078125));  // x/128 == x*2^-7 exactly
+      v1 = xmul(o, T(0.0078125));
       target = c2;
       s0 = c1;
       s1 = c2;
       s2 = c3;
       s3 = c4;
     }
-    if (CR && q >= wlo && q < whi) kaczmarz_pair(v0, v1, target, proj_diag);
+    if (CR && q >= wlo && q < whi) kaczmarz_pair(v0, v1, target, kz);
+  }
+
+  // interior-only make (no boundary rows; CR pair always inside the window)
+  __device__ __forceinline__ void make_fast(const Raw<T>& r, T& v0, T& v1) {
+    T target = r.g;
+    if (SRC == SRC_LOAD) {
+      v0 = r.a0;
+      v1 = r.a1;
+    } else if (SRC == SRC_CORR) {
+      T c1 = xsub(r.h, xmul(T(0.5), xadd(r.a0, r.a1)));
+      v0 = xadd(s2, xmul(T(0.25), xadd(s0, xmul(T(3), s1))));
+      v1 = xadd(s3, xmul(T(0.25), xadd(xmul(T(3), s1), c1)));
+      s0 = s1;
+      s1 = c1;
+      s2 = r.a0;
+      s3 = r.a1;
+    } else {
+      T e, o;
+      fmg_interior(r.h, e, o);
+      v0 = xmul(e, T(0.0078125));
+      v1 = xmul(o, T(0.0078125));
+      target = s2;
+      s0 = s1;
+      s1 = s2;
+      s2 = s3;
+      s3 = r.h;
+    }
+    if (CR) kaczmarz_pair(v0, v1, target, kz);
   }
 };
 
@@ -259,6 +403,33 @@ struct Epilogue {
       }
       Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);  // Lu[2j]
     }
+    up2 = a;
+    up1 = b;
+    Rm2 = Rm1;
+    Rm1 = Rj;
+    Rfm1 = Rfj;
+    cnt++;
+  }
+
+  // steady-state push (cnt >= 2, coarse cell j-1 interior): pointer-walking
+  // version of push() for the chain's fast loop; call fast_begin(j) first.
+  T* puH;
+  T* pfH;
+  __device__ __forceinline__ void fast_begin(i64 j) {
+    puH = uH_out ? uH_out + j * ld : nullptr;
+    pfH = fH_out + (j - 1) * ld;
+  }
+  __device__ __forceinline__ void push_fast(T a, T b, T f0, T f1, bool store) {
+    T Rj = xmul(T(0.5), xadd(a, b));
+    T Rfj = xmul(T(0.5), xadd(f0, f1));
+    if (write_uH && store) *puH = Rj;
+    puH += ld;
+    T Lodd = xmul(xsub(xsub(xmul(T(2), up1), up2), a), inv_h2);
+    T RL = xmul(T(0.5), xadd(Lprev, Lodd));
+    T LH = xmul(xsub(xsub(xmul(T(2), Rm1), Rm2), Rj), inv_H2);
+    if (store) *pfH = xadd(Rfm1, xsub(LH, RL));
+    pfH += ld;
+    Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);
     up2 = a;
     up1 = b;
     Rm2 = Rm1;

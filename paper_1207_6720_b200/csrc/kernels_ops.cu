@@ -269,13 +269,13 @@ __global__ void k_gs_sweep(T* u, const T* __restrict__ f, i64 n, i64 ld, int B, 
 // independently (the sweep direction cannot change the result).
 template <typename T>
 __global__ void k_kaczmarz(T* u, const T* __restrict__ uc, i64 j0, i64 j1, i64 ld, int B,
-                           T proj_diag) {
+                           KzCoef<T> kz) {
   int r = blockIdx.x * TX + threadIdx.x;
   if (r >= B) return;
   ROWS_LOOP(k, j1 - j0) {
     i64 j = j0 + k;
     T a = u[(2 * j) * ld + r], b = u[(2 * j + 1) * ld + r];
-    kaczmarz_pair(a, b, uc[j * ld + r], proj_diag);
+    kaczmarz_pair(a, b, uc[j * ld + r], kz);
     u[(2 * j) * ld + r] = a;
     u[(2 * j + 1) * ld + r] = b;
   }
@@ -395,7 +395,12 @@ void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i
   require(0 <= start && start <= stop && stop <= n, "kaczmarz_sweep: window outside [0, n]");
   i64 j0 = start / 2, j1 = stop / 2;
   if (j1 <= j0) return;
-  k_kaczmarz<T><<<grid_for(j1 - j0, B), dim3(TX, TY), 0, s>>>(u, uc, j0, j1, ld, B, (T)proj_diag);
+  KzCoef<T> kz;
+  int e;
+  kz.proj_diag = (T)proj_diag;
+  kz.pow2 = std::frexp(proj_diag, &e) == 0.5;
+  kz.recip = (T)(kz.pow2 ? std::ldexp(1.0, 1 - e) : 1.0 / proj_diag);
+  k_kaczmarz<T><<<grid_for(j1 - j0, B), dim3(TX, TY), 0, s>>>(u, uc, j0, j1, ld, B, kz);
   check_launch("kaczmarz_sweep");
 }
 template <typename T>

@@ -10,6 +10,8 @@
 // smooth_scratch_kernel: any ns; the extended window is staged per chain in
 // a global scratch and replayed exactly as the reference does (Kaczmarz
 // pass, GS pass, direction flip per repetition, owned write-back).
+#include <cmath>
+
 #include "fmgsr_chain.cuh"
 #include "fmgsr_internal.h"
 
@@ -20,7 +22,8 @@ struct VisitArgs {
   i64 n, ld, W, b, P, nc;
   int B, nrg;
   GsCoef<T> gc;
-  T inv_H2, proj_diag;
+  KzCoef<T> kz;
+  T inv_H2;
   bool write_u;
   const T *u_src, *uH, *uc, *f;
   T *u_out, *uH_out, *fH_out, *E;
@@ -28,8 +31,17 @@ struct VisitArgs {
   const i64 *olo, *ohi, *elo, *ehi;
 };
 
-template <typename T, int SRC, bool CR, bool EPI>
-__global__ void __launch_bounds__(128) visit_kernel(const VisitArgs<T> a) {
+constexpr int VNT = 128;  // threads per block of the visit kernel
+constexpr int VD = 8;     // cp.async ring depth (pairs) per lane
+
+template <typename T, int SRC, bool CR>
+constexpr size_t visit_smem_bytes() {
+  return (size_t)VD * SrcRows<SRC, CR>::R * VNT * sizeof(T);
+}
+
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1>
+__global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 p = gw / a.nrg;
@@ -52,20 +64,29 @@ __global__ void __launch_bounds__(128) visit_kernel(const VisitArgs<T> a) {
     we = oe + a.b < a.n ? oe + a.b : a.n;
   }
 
-  PairSource<T, SRC, CR> src;
-  src.u = a.u_src ? a.u_src + rr : nullptr;
-  src.uH = a.uH ? a.uH + rr : nullptr;
-  src.uc = a.uc ? a.uc + rr : nullptr;
-  src.f = a.f + rr;
-  src.ld = a.ld;
-  src.nc = a.nc;
-  src.proj_diag = a.proj_diag;
-  src.wlo = ws >> 1;
-  src.whi = we >> 1;
-
-  T* out = a.u_out ? a.u_out + r : nullptr;
+  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD> ch;
+  ch.src.u = a.u_src ? a.u_src + rr : nullptr;
+  ch.src.uH = a.uH ? a.uH + rr : nullptr;
+  ch.src.uc = a.uc ? a.uc + rr : nullptr;
+  ch.src.f = a.f + rr;
+  ch.src.ld = a.ld;
+  ch.src.nc = a.nc;
+  ch.src.kz = a.kz;
+  ch.src.wlo = ws >> 1;
+  ch.src.whi = we >> 1;
+  ch.gc = a.gc;
+  ch.n = a.n;
+  ch.nc = a.nc;
+  ch.ld = a.ld;
+  ch.ws = ws;
+  ch.os = os;
+  ch.oe = oe;
+  ch.store = store;
+  ch.ring = reinterpret_cast<T*>(visit_smem) + threadIdx.x;
+  ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + r : nullptr;
   if (!EPI) {
-    run_chain_ns1<T, SRC, CR, false>(src, a.gc, a.n, ws, os, oe, out, a.ld, true, store, nullptr);
+    ch.epi = nullptr;
+    ch.run(we);
     return;
   }
   Epilogue<T> ep;
@@ -80,7 +101,8 @@ __global__ void __launch_bounds__(128) visit_kernel(const VisitArgs<T> a) {
   ep.nc = a.nc;
   ep.cnt = 0;
   ep.up2 = ep.up1 = ep.Lprev = ep.Rm2 = ep.Rm1 = ep.Rfm1 = T(0);
-  run_chain_ns1<T, SRC, CR, true>(src, a.gc, a.n, ws, os, oe, out, a.ld, a.write_u, store, &ep);
+  ch.epi = &ep;
+  ch.run(we);
   EdgeRec<T> right;
   ep.finish(store, right);
   const i64 ldE = (i64)a.nrg * 32;
@@ -104,11 +126,39 @@ static GsCoef<T> make_coef(i64 n, double omega) {
   return g;
 }
 
+template <typename T>
+static KzCoef<T> make_kz(double pd) {
+  KzCoef<T> k;
+  int e;
+  k.proj_diag = (T)pd;
+  k.pow2 = std::frexp(pd, &e) == 0.5;  // pd = 2^(e-1): dividing is multiplying by 2^(1-e)
+  k.recip = (T)(k.pow2 ? std::ldexp(1.0, 1 - e) : 1.0 / pd);
+  return k;
+}
+
 template <typename T, int SRC, bool CR, bool EPI>
 static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   i64 warps = a.P * a.nrg;
-  i64 blocks = (warps + 3) / 4;
-  visit_kernel<T, SRC, CR, EPI><<<(unsigned)blocks, 128, 0, s>>>(a);
+  i64 blocks = (warps + VNT / 32 - 1) / (VNT / 32);
+  constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
+  const bool om1 = a.gc.omega == T(1);
+  if (om1) {
+    auto k = visit_kernel<T, SRC, CR, EPI, true>;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+      check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      attr = true;
+    }
+    k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+  } else {
+    auto k = visit_kernel<T, SRC, CR, EPI, false>;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+      check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+      attr = true;
+    }
+    k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+  }
 }
 
 template <typename T>
@@ -124,7 +174,7 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   a.nc = d.n / 2;
   a.gc = make_coef<T>(d.n, d.omega);
   a.inv_H2 = (T)(double)((i64)1 << (2 * (level_of(d.n) - 1)));
-  a.proj_diag = (T)d.proj_diag;
+  a.kz = make_kz<T>(d.proj_diag);
   a.write_u = d.write_u;
   a.u_src = d.u_src;
   a.uH = d.uH;
@@ -191,7 +241,7 @@ struct ScratchArgs {
   i64 n, ld, W, b, P, ns, sld;
   int B, nrg;
   GsCoef<T> gc;
-  T proj_diag;
+  KzCoef<T> kz;
   const i64 *olo, *ohi, *elo, *ehi, *soff;
   const T *u_in, *f, *uc;
   T *out, *scratch;
@@ -236,7 +286,7 @@ __global__ void __launch_bounds__(128) smooth_scratch_kernel(const ScratchArgs<T
       const T* uc = a.uc + rr;
       for (i64 j = ws >> 1; j < (we >> 1); j++) {
         T x = S(2 * j), y = S(2 * j + 1);
-        kaczmarz_pair(x, y, ldg(uc + j * ld), a.proj_diag);
+        kaczmarz_pair(x, y, ldg(uc + j * ld), a.kz);
         S(2 * j) = x;
         S(2 * j + 1) = y;
       }
@@ -286,7 +336,7 @@ void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s) {
   a.sld = d.sld;
   a.ns = d.ns;
   a.gc = make_coef<T>(d.n, d.omega);
-  a.proj_diag = (T)d.proj_diag;
+  a.kz = make_kz<T>(d.proj_diag);
   a.olo = d.olo;
   a.ohi = d.ohi;
   a.elo = d.elo;

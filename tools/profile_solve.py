@@ -1,0 +1,31 @@
+"""Run a few FMG solves op by op (no CUDA graph) for ncu: every level visit is
+its own launch in a deterministic order.
+
+    python tools/profile_solve.py [--workload config2] [--solves 1] [--graph]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1207_6720_b200 as fm  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="config2")
+ap.add_argument("--solves", type=int, default=1)
+ap.add_argument("--graph", action="store_true")
+a = ap.parse_args()
+w = bench.WORKLOADS[a.workload]
+dt = torch.float64 if w["dtype"] == "f64" else torch.float32
+cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
+                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, use_graph=a.graph))
+f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+sol = torch.empty_like(f)
+for _ in range(a.solves):
+    plan.solve(f, sol)
+torch.cuda.synchronize()
+print("solves done", a.solves, plan.info())

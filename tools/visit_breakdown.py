@@ -1,0 +1,45 @@
+"""Per-level-visit device times of one FMG pass (op-by-op launches with CUDA
+events on the launching stream), summed by level and kind.
+
+    python tools/visit_breakdown.py [--workload config2] [--reps 3] [--unfused]
+"""
+import argparse
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1207_6720_b200 as fm  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="config2")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--unfused", action="store_true")
+a = ap.parse_args()
+w = bench.WORKLOADS[a.workload]
+dt = torch.float64 if w["dtype"] == "f64" else torch.float32
+cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
+                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused))
+f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+sol = torch.empty_like(f)
+for _ in range(2):
+    plan.solve(f, sol)
+torch.cuda.synchronize()
+acc = collections.defaultdict(float)
+cnt = collections.defaultdict(int)
+for _ in range(a.reps):
+    for kind, lvl, ms in plan.solve_timed(f, sol):
+        acc[(lvl, kind)] += ms / a.reps
+        cnt[(lvl, kind)] += 1
+tot = sum(acc.values())
+print(f"workload {a.workload} fused={not a.unfused}: sum of visit times {tot:.3f} ms")
+for (lvl, kind) in sorted(acc, key=lambda k: (-k[0], k[1])):
+    n = cnt[(lvl, kind)] // a.reps
+    print(f"  level {lvl:2d} {kind:7s} x{n:3d}  {acc[(lvl, kind)]:8.3f} ms  {100*acc[(lvl, kind)]/tot:5.1f}%"
+          f"  per-visit {acc[(lvl, kind)]/max(n,1)*1e3:8.1f} us")
+print(json.dumps(plan.info()))
