@@ -143,6 +143,8 @@ typedef struct fmgsr_plan_desc {
   double omega;       /* relaxation weight (reference: 1.0) */
   int32_t fused;      /* 1: fused level visits where eligible; 0: operator-by-operator */
   int32_t use_graph;  /* 1: capture the cycle in a CUDA graph per (in, out) pair */
+  int32_t coarse;     /* on-chip coarse hierarchy (fused, ns = 1 only): -1 auto cutoff,
+                         0 off, k > 0: cutoff level Lc = k - 1 (capped by the smem budget) */
 } fmgsr_plan_desc;
 
 typedef struct fmgsr_plan_info {
@@ -151,6 +153,8 @@ typedef struct fmgsr_plan_info {
   int64_t visits_per_solve;     /* level visits (smooths + direct solves) */
   double alg_bytes_per_solve;   /* compulsory HBM traffic model */
   double finest_visit_alg_bytes;/* algorithmic bytes of one finest-level visit */
+  int32_t coarse_cutoff;        /* Lc of the on-chip coarse hierarchy, -1 if unused */
+  int32_t coarse_columns;       /* RHS columns per coarse CTA */
 } fmgsr_plan_info;
 
 int fmgsr_plan_create(const fmgsr_plan_desc* desc, void** plan);

@@ -31,7 +31,7 @@ class PlanDesc(C.Structure):
         ("m0", _i32), ("m", _i32), ("n_sr", _i32), ("ns", _i32),
         ("geom_mode", _i32), ("dtype", _i32),
         ("P", _i64), ("b", _i64), ("B", _i64), ("ld", _i64),
-        ("omega", _d), ("fused", _i32), ("use_graph", _i32),
+        ("omega", _d), ("fused", _i32), ("use_graph", _i32), ("coarse", _i32),
     ]
 
 
@@ -39,7 +39,7 @@ class PlanInfo(C.Structure):
     _fields_ = [
         ("workspace_bytes", _i64), ("launches_per_solve", _i64),
         ("visits_per_solve", _i64), ("alg_bytes_per_solve", _d),
-        ("finest_visit_alg_bytes", _d),
+        ("finest_visit_alg_bytes", _d), ("coarse_cutoff", _i32), ("coarse_columns", _i32),
     ]
 
 

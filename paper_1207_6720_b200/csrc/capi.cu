@@ -36,7 +36,7 @@ static void check_field(i64 n, i64 B, i64 ld, const char* what) {
 // ===========================================================================
 // Plan
 // ===========================================================================
-enum VisitKind { VK_TOP = 0, VK_DOWN = 1, VK_UP = 2, VK_DIRECT = 3, VK_CASCADE = 4 };
+enum VisitKind { VK_TOP = 0, VK_DOWN = 1, VK_UP = 2, VK_DIRECT = 3, VK_CASCADE = 4, VK_COARSE = 5 };
 
 struct LevelGeo {
   i64 W, b;
@@ -85,6 +85,9 @@ struct Plan : PlanBase {
   std::vector<cudaEvent_t> ev;
   std::vector<int32_t> ev_lvl, ev_kind;
   bool timing = false;
+  // coarse hierarchy kernel: levels m0..Lc on chip, CW RHS columns per CTA
+  bool use_coarse = false;
+  int Lc = 0, CW = 1;
 
   bool is_sr(int l) const { return l > d.m - d.n_sr; }
 
@@ -142,6 +145,17 @@ struct Plan : PlanBase {
       }
     }
     check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
+    // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
+    // three fields per level (two u, f) for CW columns fit in ~200 KB.
+    use_coarse = d.fused && d.ns == 1 && d.coarse != 0;
+    if (use_coarse) {
+      i64 cw = 1;
+      while (cw * 2 <= 32 && cw * 2 * 128 <= d.B) cw *= 2;
+      CW = (int)cw;
+      Lc = m0;
+      while (Lc + 1 <= m - 1 && coarse_smem_bytes<T>(m0, Lc + 1, CW) <= 200 * 1024) Lc++;
+      if (d.coarse > 0 && d.coarse - 1 >= m0 && d.coarse - 1 < Lc) Lc = d.coarse - 1;
+    }
   }
 
   ~Plan() override {
@@ -357,15 +371,22 @@ struct Plan : PlanBase {
       check_cuda(cudaMemsetAsync(cnt_all, 0, cnt_bytes, s), "counter reset");
       n_launch++;
     }
-    // f cascade (cycles.py:178-180)
+    // f cascade (cycles.py:178-180): up to 6 levels per launch
     mark_begin(s, m, VK_CASCADE);
-    for (int k = m - 1; k >= m0; k--) {
-      const T* src = (k == m - 1) ? forcing : lv[k + 1].f;
-      launch_restrict(src, lv[k].f, (i64)2 << k, d.ld, (int)d.B, s);
+    for (int k = m - 1; k >= m0;) {
+      CascadeDst<T> cd;
+      const int src_l = k + 1;
+      const T* src = (src_l == m) ? forcing : lv[src_l].f;
+      while (cd.levels < 6 && k >= m0) cd.p[cd.levels++] = lv[k--].f;
+      launch_cascade(src, (i64)1 << src_l, cd, d.ld, (int)d.B, s);
       n_launch++;
     }
     mark_end(s);
     n_visit--;  // the cascade is not a level visit
+    if (use_coarse) {
+      enqueue_coarse(forcing, solution, s);
+      return;
+    }
     visit_direct(s);  // cycles.py:183
     for (int k = m0; k < m; k++) {
       const int t = k + 1;
@@ -374,6 +395,59 @@ struct Plan : PlanBase {
       for (int l = t - 1; l > m0; l--) visit_down(l, s);   // cycles.py:99-105
       visit_direct(s);                                     // smooth_level at m0
       for (int l = m0 + 1; l <= t; l++) {                  // cycles.py:118-133
+        const T* fl = (l == m) ? forcing : lv[l].f;
+        visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s);
+      }
+    }
+  }
+
+  CoarseArgs<T> coarse_args(int mode) const {
+    CoarseArgs<T> a;
+    a.m0 = d.m0;
+    a.Lc = Lc;
+    a.m = d.m;
+    a.n_sr = d.n_sr;
+    a.mode = mode;
+    a.CW = CW;
+    a.B = (int)d.B;
+    a.ld = d.ld;
+    for (int l = d.m0; l <= Lc; l++) {
+      a.W[l] = lv[l].W;
+      a.b[l] = lv[l].b;
+      a.forig[l] = lv[l].f;
+    }
+    a.omega = d.omega;
+    a.kz.proj_diag = (T)0.5;
+    a.kz.recip = (T)2.0;
+    a.kz.pow2 = true;
+    return a;
+  }
+
+  // Schedule with levels m0..Lc resident in one CTA per column group: one
+  // launch for FMG steps m0+1..Lc, then per step t > Lc the grid visits of
+  // levels > Lc around one coarse launch for the V-cycle below Lc+1.
+  void enqueue_coarse(const T* forcing, T* solution, cudaStream_t s) {
+    const int m = d.m;
+    {
+      mark_begin(s, Lc, VK_COARSE);
+      CoarseArgs<T> a = coarse_args(0);
+      a.u_top = lv[Lc].u[lv[Lc].cur];
+      launch_coarse(a, s);
+      n_launch++;
+      mark_end(s);
+    }
+    for (int t = Lc + 1; t <= m; t++) {
+      const T* ft = (t == m) ? forcing : lv[t].f;
+      visit_top(t, ft, s);
+      for (int l = t - 1; l > Lc; l--) visit_down(l, s);
+      mark_begin(s, Lc, VK_COARSE);
+      CoarseArgs<T> a = coarse_args(1);
+      a.u_top = lv[Lc].u[lv[Lc].cur];  // restricted u_{Lc} in, V-cycled u_{Lc} out (in place)
+      a.f_top = lv[Lc].f;
+      launch_coarse(a, s);
+      n_launch++;
+      mark_end(s);
+      for (int l = Lc + 1; l <= t; l++) {
         const T* fl = (l == m) ? forcing : lv[l].f;
         visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s);
       }
@@ -466,6 +540,8 @@ struct Plan : PlanBase {
     inf->visits_per_solve = visits;
     inf->alg_bytes_per_solve = w * (double)d.B * sizeof(T);
     inf->finest_visit_alg_bytes = words_visit(VK_UP, m) * (double)d.B * sizeof(T);
+    inf->coarse_cutoff = use_coarse ? Lc : -1;
+    inf->coarse_columns = use_coarse ? CW : 0;
   }
 };
 

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fmgsr_internal.h"
+
 namespace fmgsr {
 
 typedef int64_t i64;
@@ -77,12 +79,6 @@ __device__ __forceinline__ T gs_cell(const GsCoef<T>& c, i64 i, i64 n, T uL, T u
 // _kernels_numba.py:53-56: r = uc - 0.5(a+b); t = r/proj_diag; a,b += 0.5 t.
 // When proj_diag is a power of two (the reference's 0.5) the division is an
 // exact multiply by its reciprocal.
-template <typename T>
-struct KzCoef {
-  T proj_diag, recip;
-  bool pow2;
-};
-
 template <typename T>
 __device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, const KzCoef<T>& k) {
   T r = xsub(uc, xmul(T(0.5), xadd(a, b)));

@@ -56,6 +56,40 @@ int guarded(F&& f) {
   }
 }
 
+// Kaczmarz divisor: proj_diag, and its exact reciprocal when a power of two
+template <typename T>
+struct KzCoef {
+  T proj_diag, recip;
+  bool pow2;
+};
+
+// Coarse hierarchy kernel (kernels_coarse.cu): one CTA per CW RHS columns
+// runs every visit of levels m0..Lc out of shared memory.
+template <typename T>
+struct CoarseArgs {
+  int m0 = 0, Lc = 0, m = 0, n_sr = 0;
+  int mode = 0;  // 0: coarse FMG steps m0+1..Lc; 1: V-cycle segment below Lc+1
+  int CW = 1, B = 1;
+  i64 ld = 0;
+  i64 W[32] = {}, b[32] = {};
+  const T* forig[32] = {};  // mode 0: restricted forcing per level
+  const T* f_top = nullptr;  // mode 1: f_{Lc}
+  T* u_top = nullptr;        // mode 1: in/out u_{Lc}; mode 0: out
+  double omega = 1.0;
+  KzCoef<T> kz{};
+};
+template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
+template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW);
+
+// Multi-level restriction (f cascade): p[k] receives level (src_level-1-k)
+template <typename T>
+struct CascadeDst {
+  T* p[6] = {};
+  int levels = 0;
+};
+template <typename T>
+void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, int B, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // Level-visit descriptor (uniform patch geometry: owned width W, buffer b).
 // ---------------------------------------------------------------------------

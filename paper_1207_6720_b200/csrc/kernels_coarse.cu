@@ -1,0 +1,410 @@
+// kernels_coarse.cu -- the coarse end of the hierarchy, resident on chip.
+//
+// Below a cutoff level Lc every level visit of the FMG cycle is a few
+// microseconds of latency-bound work, so launching one grid per visit (the
+// reference's horizontal order) would be dominated by launch and pipeline
+// fill.  Right-hand sides are independent, so one CTA owns a group of CW RHS
+// columns and runs *all* visits of levels m0..Lc for them out of shared
+// memory, separated only by __syncthreads():
+//   mode 0 (coarse FMG): the coarsest direct solve and FMG steps m0+1..Lc
+//                        (reference cycles.py:178-199 for those levels);
+//   mode 1 (V segment) : for a step t > Lc, the part of the V-cycle below
+//                        Lc+1: down leg Lc..m0+1, direct solve, up leg
+//                        m0+1..Lc (cycles.py:95-134).
+// Operators are the exact-order device functions shared with the grid
+// kernels, so results stay bit-identical to the reference.
+//
+// The same launch also hosts the multi-level restriction of the forcing
+// (the f cascade, cycles.py:178-180).
+#include <cmath>
+
+#include "fmgsr_device.cuh"
+#include "fmgsr_internal.h"
+
+namespace fmgsr {
+
+namespace {
+
+constexpr int CNT = 512;  // threads per coarse CTA
+
+template <typename T>
+__device__ __forceinline__ T pow4(int l) {
+  return (T)(double)((i64)1 << (2 * l));
+}
+
+// Shared-memory layout of the coarse hierarchy for CW columns: level l keeps
+// u0, u1, f (n_l x CW each, cell-major, column fastest) at offset
+// 3 CW (2^l - 2^m0); a level's current u buffer is one bit of `curmask`.
+// Everything is addressed arithmetically (no per-level tables), so nothing
+// spills to local memory.
+template <typename T, int CW>
+struct CoarseCtx {
+  const CoarseArgs<T>& a;
+  T* sm;
+  const T* dfac;  // direct-solve factor d[n0], e[n0]
+  const T* efac;
+  int c0;
+  unsigned curmask;
+  __device__ CoarseCtx(const CoarseArgs<T>& args) : a(args) {}
+
+  __device__ __forceinline__ int nlev(int l) const { return 1 << l; }
+  __device__ __forceinline__ T* U(int l, int w) const {
+    return sm + 3 * CW * ((1 << l) - (1 << a.m0)) + w * CW * (1 << l);
+  }
+  __device__ __forceinline__ T* Fl(int l) const { return U(l, 2); }
+  __device__ __forceinline__ int cur(int l) const { return (curmask >> l) & 1; }
+  __device__ __forceinline__ void flip(int l) { curmask ^= 1u << l; }
+  __device__ __forceinline__ void set0(int l) { curmask &= ~(1u << l); }
+
+  __device__ bool sr(int l) const { return l > a.m - a.n_sr; }
+
+  __device__ void load(T* dst, const T* src, int n) {
+    for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
+      int i = e / CW, c = e % CW, col = c0 + c;
+      dst[e] = col < a.B ? src[(i64)i * a.ld + col] : T(0);
+    }
+  }
+  __device__ void store(T* dst, const T* src, int n) {
+    for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
+      int i = e / CW, c = e % CW, col = c0 + c;
+      if (col < a.B) dst[(i64)i * a.ld + col] = src[e];
+    }
+  }
+
+  // prolong_fmg, stencils.py:67-105: dst level l (nf cells) from src level l-1
+  __device__ void prolong(T* dst, const T* src, int nc) {
+    const int nf = 2 * nc;
+    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x) {
+      int i = e / CW, c = e % CW;
+      const T* s = src + c;
+#define C(k) s[(k) * CW]
+      T v;
+      if (i >= 4 && i < nf - 4) {
+        if ((i & 1) == 0) {
+          int q = i / 2;
+          v = xsub(xadd(xadd(xmul(T(-5), C(q - 2)), xmul(T(35), C(q - 1))), xmul(T(105), C(q))),
+                   xmul(T(7), C(q + 1)));
+        } else {
+          int q = (i - 1) / 2;
+          v = xsub(xadd(xadd(xmul(T(-7), C(q - 1)), xmul(T(105), C(q))), xmul(T(35), C(q + 1))),
+                   xmul(T(5), C(q + 2)));
+        }
+      } else if (i == 0) v = xsub(xmul(T(70), C(0)), xmul(T(2), C(1)));
+      else if (i == 1) v = xsub(xadd(xmul(T(112), C(0)), xmul(T(35), C(1))), xmul(T(5), C(2)));
+      else if (i == 2) v = xsub(xadd(xmul(T(40), C(0)), xmul(T(105), C(1))), xmul(T(7), C(2)));
+      else if (i == 3)
+        v = xsub(xadd(xadd(xmul(T(-7), C(0)), xmul(T(105), C(1))), xmul(T(35), C(2))),
+                 xmul(T(5), C(3)));
+      else if (i == nf - 4)
+        v = xsub(xadd(xadd(xmul(T(-7), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(35), C(nc - 3))),
+                 xmul(T(5), C(nc - 4)));
+      else if (i == nf - 3)
+        v = xsub(xadd(xmul(T(40), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(7), C(nc - 3)));
+      else if (i == nf - 2)
+        v = xsub(xadd(xmul(T(112), C(nc - 1)), xmul(T(35), C(nc - 2))), xmul(T(5), C(nc - 3)));
+      else v = xsub(xmul(T(70), C(nc - 1)), xmul(T(2), C(nc - 2)));
+#undef C
+      dst[e] = xmul(v, T(0.0078125));
+    }
+  }
+
+  // cycles.py:120-121: dst = u + P(uH - R u), u on level with nf cells
+  __device__ void correct(T* dst, const T* u, const T* uH, int nf) {
+    const int nc = nf / 2;
+    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x) {
+      int i = e / CW, c = e % CW;
+      const T* ur = u + c;
+      const T* hr = uH + c;
+      auto cc = [&](int j) {
+        return xsub(hr[j * CW], xmul(T(0.5), xadd(ur[(2 * j) * CW], ur[(2 * j + 1) * CW])));
+      };
+      T p;
+      if (i == 0) p = xmul(T(0.5), cc(0));
+      else if (i == nf - 1) p = xmul(T(0.5), cc(nc - 1));
+      else if (i & 1) {
+        int j = (i - 1) / 2;
+        p = xmul(T(0.25), xadd(xmul(T(3), cc(j)), cc(j + 1)));
+      } else {
+        int j = (i - 2) / 2;
+        p = xmul(T(0.25), xadd(cc(j), xmul(T(3), cc(j + 1))));
+      }
+      dst[e] = xadd(ur[i * CW], p);
+    }
+  }
+
+  // restrict + coarse_rhs (stencils.py:39-47, 108-125), level l -> l-1
+  __device__ void restrict_tau(const T* u, const T* f, T* uH, T* fH, int nf, int l) {
+    const int nc = nf / 2;
+    const T ih = pow4<T>(l), iH = pow4<T>(l - 1);
+    for (int e = threadIdx.x; e < nc * CW; e += blockDim.x) {
+      int j = e / CW, c = e % CW;
+      const T* ur = u + c;
+      auto ru = [&](int k) { return xmul(T(0.5), xadd(ur[(2 * k) * CW], ur[(2 * k + 1) * CW])); };
+      auto lu = [&](int i) {
+        T s;
+        if (i == 0) s = xsub(xmul(T(3), ur[0]), ur[CW]);
+        else if (i == nf - 1) s = xsub(xmul(T(3), ur[(nf - 1) * CW]), ur[(nf - 2) * CW]);
+        else s = xsub(xsub(xmul(T(2), ur[i * CW]), ur[(i - 1) * CW]), ur[(i + 1) * CW]);
+        return xmul(s, ih);
+      };
+      T Rj = ru(j);
+      T LH;
+      if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru(1)), iH);
+      else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rj), ru(nc - 2)), iH);
+      else LH = xmul(xsub(xsub(xmul(T(2), Rj), ru(j - 1)), ru(j + 1)), iH);
+      T RL = xmul(T(0.5), xadd(lu(2 * j), lu(2 * j + 1)));
+      T Rf = xmul(T(0.5), xadd(f[(2 * j) * CW + c], f[(2 * j + 1) * CW + c]));
+      fH[e] = xadd(Rf, xsub(LH, RL));
+      uH[e] = Rj;
+    }
+  }
+
+  // additive patch smoother, ns = 1 (_kernels_numba.py:60-92), one chain per
+  // (patch, column); Kaczmarz applied per cell from the unmodified input
+  __device__ void smooth(int l, const T* uin, const T* f, const T* uc, T* out) {
+    const int n = nlev(l), W = (int)a.W[l], b = (int)a.b[l];
+    const int P = n / W;
+    GsCoef<T> gc;
+    gc.inv_h2 = pow4<T>(l);
+    gc.rdiag = (T)(1.0 / (2.0 * (double)((i64)1 << (2 * l))));
+    gc.diag_b = xmul(T(3), gc.inv_h2);
+    gc.omega = (T)a.omega;
+    for (int k = threadIdx.x; k < P * CW; k += blockDim.x) {
+      const int p = k / CW, c = k % CW;
+      const int os = p * W, oe = os + W;
+      const int ws = os - b > 0 ? os - b : 0;
+      const int we = oe + b < n ? oe + b : n;
+      const int wlo = ws >> 1, whi = we >> 1;
+      const T* ui = uin + c;
+      const T* fc = f + c;
+      T* oc = out + c;
+      auto val = [&](int x) -> T {
+        T v = ui[x * CW];
+        if (uc) {
+          int j = x >> 1;
+          if (j >= wlo && j < whi) {
+            T aa = ui[(2 * j) * CW], bb = ui[(2 * j + 1) * CW];
+            kaczmarz_pair(aa, bb, uc[j * CW + c], a.kz);
+            v = (x & 1) ? bb : aa;
+          }
+        }
+        return v;
+      };
+      T uL = ws > 0 ? val(ws - 1) : T(0);
+      T cu = val(ws);
+      T nx = (ws + 1 < n) ? val(ws + 1) : T(0);
+      for (int i = ws; i < oe; i++) {
+        T nn = (i + 2 < n) ? val(i + 2) : T(0);  // one cell of lookahead beyond nx
+        T v = gs_cell(gc, (i64)i, (i64)n, uL, cu, nx, fc[i * CW]);
+        if (i >= os) oc[i * CW] = v;
+        uL = v;
+        cu = nx;
+        nx = nn;
+      }
+    }
+  }
+
+  // LAPACK ?ptsv order (smoothers.py:210-225): dptts2 with the shared factor
+  __device__ void direct(const T* f, T* u) {
+    const int n = nlev(a.m0);
+    for (int c = threadIdx.x; c < CW; c += blockDim.x) {
+      T prev = f[c];
+      u[c] = prev;
+      for (int i = 1; i < n; i++) {
+        prev = xsub(f[i * CW + c], xmul(prev, efac[i - 1]));
+        u[i * CW + c] = prev;
+      }
+      T nx = xdiv(prev, dfac[n - 1]);
+      u[(n - 1) * CW + c] = nx;
+      for (int i = n - 2; i >= 0; i--) {
+        nx = xsub(xdiv(u[i * CW + c], dfac[i]), xmul(nx, efac[i]));
+        u[i * CW + c] = nx;
+      }
+    }
+  }
+
+  // ---- level visits (each ends with a barrier) ---------------------------------
+  __device__ void visit_top(int t) {  // Pi, pre-smooth, restrict + tau
+    int h = cur(t - 1);
+    prolong(U(t, 1), U(t - 1, h), nlev(t - 1));
+    __syncthreads();
+    smooth(t, U(t, 1), Fl(t), nullptr, U(t, 0));
+    set0(t);
+    __syncthreads();
+    restrict_tau(U(t, 0), Fl(t), U(t - 1, h ^ 1), Fl(t - 1), nlev(t), t);
+    flip(t - 1);
+    __syncthreads();
+  }
+  __device__ void visit_down(int l) {
+    int c = cur(l);
+    smooth(l, U(l, c), Fl(l), nullptr, U(l, c ^ 1));
+    flip(l);
+    __syncthreads();
+    int h = cur(l - 1);
+    restrict_tau(U(l, c ^ 1), Fl(l), U(l - 1, h ^ 1), Fl(l - 1), nlev(l), l);
+    flip(l - 1);
+    __syncthreads();
+  }
+  __device__ void visit_direct() {
+    int c = cur(a.m0);
+    direct(Fl(a.m0), U(a.m0, c ^ 1));
+    flip(a.m0);
+    __syncthreads();
+  }
+  __device__ void visit_up(int l) {
+    int c = cur(l);
+    const T* uH = U(l - 1, cur(l - 1));
+    const bool s = sr(l);
+    if (s) prolong(U(l, c ^ 1), uH, nlev(l - 1));
+    else correct(U(l, c ^ 1), U(l, c), uH, nlev(l));
+    __syncthreads();
+    smooth(l, U(l, c ^ 1), Fl(l), s ? uH : nullptr, U(l, c));
+    __syncthreads();
+  }
+};
+
+template <typename T, int CW>
+__global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char coarse_smem[];
+  CoarseCtx<T, CW> x(a);
+  x.sm = reinterpret_cast<T*>(coarse_smem);
+  x.c0 = blockIdx.x * CW;
+  x.curmask = 0;
+  const int m0 = a.m0, Lc = a.Lc;
+  const int n0 = 1 << m0;
+  T* d = x.sm + 3 * CW * ((1 << (Lc + 1)) - (1 << m0));
+  T* e = d + n0;
+  if (threadIdx.x == 0) {  // dpttrf, as in k_direct_solve
+    T ih = pow4<T>(m0);
+    for (int i = 0; i < n0; i++) d[i] = xmul(T(2), ih);
+    d[0] = xmul(T(3), ih);
+    d[n0 - 1] = xmul(T(3), ih);
+    for (int i = 0; i < n0 - 1; i++) e[i] = -ih;
+    for (int i = 0; i < n0 - 1; i++) {
+      T ei = e[i];
+      e[i] = xdiv(ei, d[i]);
+      d[i + 1] = xsub(d[i + 1], xmul(e[i], ei));
+    }
+  }
+  x.dfac = d;
+  x.efac = e;
+  if (a.mode == 0) {
+    x.load(x.Fl(m0), a.forig[m0], n0);
+    __syncthreads();
+    x.visit_direct();
+    for (int t = m0 + 1; t <= Lc; t++) {
+      x.load(x.Fl(t), a.forig[t], 1 << t);
+      __syncthreads();
+      x.visit_top(t);
+      for (int l = t - 1; l > m0; l--) x.visit_down(l);
+      x.visit_direct();
+      for (int l = m0 + 1; l <= t; l++) x.visit_up(l);
+    }
+  } else {
+    x.load(x.U(Lc, 0), a.u_top, 1 << Lc);
+    x.load(x.Fl(Lc), a.f_top, 1 << Lc);
+    __syncthreads();
+    for (int l = Lc; l > m0; l--) x.visit_down(l);
+    x.visit_direct();
+    for (int l = m0 + 1; l <= Lc; l++) x.visit_up(l);
+  }
+  x.store(a.u_top, x.U(Lc, x.cur(Lc)), 1 << Lc);
+}
+
+// f cascade: each thread restricts 2^S consecutive rows of one column down S
+// levels with a binary-counter stack, pairing (left, right) exactly like
+// restrict() applied level by level (stencils.py:39-47).
+template <typename T, int S>
+__global__ void k_cascade(const T* __restrict__ src, CascadeDst<T> dst, i64 n_src, i64 ld, int B) {
+  int r = blockIdx.x * 32 + threadIdx.x;
+  if (r >= B) return;
+  const i64 nblk = n_src >> S;
+  for (i64 blk = (i64)blockIdx.y * blockDim.y + threadIdx.y; blk < nblk;
+       blk += (i64)gridDim.y * blockDim.y) {
+    const T* s = src + (blk << S) * ld + r;
+    T stack[S];
+#pragma unroll
+    for (int i = 0; i < (1 << S); i++) {
+      T v = s[(i64)i * ld];
+#pragma unroll
+      for (int k = 0; k < S; k++) {
+        // at step i, level k+1 completes iff the low k+1 bits of i are all ones
+        if (((i >> k) & 1) == 0) {
+          stack[k] = v;
+          break;
+        }
+        v = xmul(T(0.5), xadd(stack[k], v));
+        i64 idx = ((blk << S) + i) >> (k + 1);
+        dst.p[k][idx * ld + r] = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T>
+size_t coarse_smem_bytes(int m0, int Lc, int CW) {
+  i64 cells = 0;
+  for (int l = m0; l <= Lc; l++) cells += (i64)1 << l;
+  return (size_t)(3 * cells * CW + 2 * ((i64)1 << m0)) * sizeof(T);
+}
+
+template <typename T, int CW>
+static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    check_cuda(cudaFuncSetAttribute(coarse_kernel<T, CW>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+               "coarse smem attr");
+    attr = true;
+  }
+  unsigned blocks = (unsigned)((a.B + CW - 1) / CW);
+  coarse_kernel<T, CW><<<blocks, CNT, smem, s>>>(a);
+}
+
+template <typename T>
+void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
+  require(a.Lc >= a.m0 && a.Lc < 31, "coarse: bad cutoff");
+  size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW);
+  require(smem <= 227 * 1024, "coarse: shared memory budget exceeded");
+  switch (a.CW) {
+    case 1: launch_coarse_cw<T, 1>(a, smem, s); break;
+    case 2: launch_coarse_cw<T, 2>(a, smem, s); break;
+    case 4: launch_coarse_cw<T, 4>(a, smem, s); break;
+    case 8: launch_coarse_cw<T, 8>(a, smem, s); break;
+    case 16: launch_coarse_cw<T, 16>(a, smem, s); break;
+    case 32: launch_coarse_cw<T, 32>(a, smem, s); break;
+    default: require(false, "coarse: column group must be a power of two <= 32");
+  }
+  check_launch("coarse_kernel");
+}
+
+template <typename T>
+void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, int B,
+                    cudaStream_t s) {
+  require(dst.levels >= 1 && dst.levels <= 6, "cascade: 1..6 levels per launch");
+  require((n_src >> dst.levels) >= 1, "cascade: too many levels");
+  dim3 block(32, 4);
+  i64 blocks_y = ((n_src >> dst.levels) + 3) / 4;
+  if (blocks_y > 16384) blocks_y = 16384;
+  dim3 grid((unsigned)((B + 31) / 32), (unsigned)blocks_y);
+  switch (dst.levels) {
+    case 1: k_cascade<T, 1><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 2: k_cascade<T, 2><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 3: k_cascade<T, 3><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 4: k_cascade<T, 4><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 5: k_cascade<T, 5><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    default: k_cascade<T, 6><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+  }
+  check_launch("cascade");
+}
+
+template size_t coarse_smem_bytes<double>(int, int, int);
+template size_t coarse_smem_bytes<float>(int, int, int);
+template void launch_coarse<double>(const CoarseArgs<double>&, cudaStream_t);
+template void launch_coarse<float>(const CoarseArgs<float>&, cudaStream_t);
+template void launch_cascade<double>(const double*, i64, const CascadeDst<double>&, i64, int, cudaStream_t);
+template void launch_cascade<float>(const float*, i64, const CascadeDst<float>&, i64, int, cudaStream_t);
+
+}  // namespace fmgsr

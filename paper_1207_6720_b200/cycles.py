@@ -145,12 +145,16 @@ def _operator_path(cfg, forcing, collect_diagnostics, debug_sr):
 
 
 def fmg_solve(cfg: SolverConfig, forcing, exact=None, collect_diagnostics: bool = False,
-              debug_sr: bool = False, keep_state: bool = False, fused: bool = True):
+              debug_sr: bool = False, keep_state: bool = False, fused: bool = True,
+              coarse: int = -1):
     """One full-multigrid pass (cycles.py:137-222) for one or B right-hand sides.
 
     ``forcing`` is (2**m,) or (2**m, B).  Returns (solution, Diagnostics).
     ``diag.rel_error`` is the plain relative L2 error against ``exact`` (the
-    maximum over right-hand sides for a batch).
+    maximum over right-hand sides for a batch).  ``fused`` / ``coarse`` select
+    the native plan's kernels (fused level visits; on-chip coarse hierarchy
+    with automatic cutoff (-1), off (0) or cutoff level ``coarse - 1``); all
+    choices give bit-identical results.
     """
     m = cfg.hierarchy.m
     if F.length(forcing) != 2 ** m:
@@ -163,7 +167,7 @@ def fmg_solve(cfg: SolverConfig, forcing, exact=None, collect_diagnostics: bool 
         if keep_state:
             diag.state = state
     else:
-        plan = get_plan(key_from_config(cfg, Fd.B, dt, fused=fused))
+        plan = get_plan(key_from_config(cfg, Fd.B, dt, fused=fused, coarse=coarse))
         sol = plan.solve(f)
         diag = Diagnostics()
     if exact is not None:

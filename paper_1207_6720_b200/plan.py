@@ -34,10 +34,11 @@ class PlanKey:
     omega: float
     fused: bool = True
     use_graph: bool = True
+    coarse: int = -1  # on-chip coarse hierarchy: -1 auto, 0 off, k > 0 cutoff level k - 1
 
 
 def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
-                    use_graph: bool = True) -> PlanKey:
+                    use_graph: bool = True, coarse: int = -1) -> PlanKey:
     """PlanKey of a ``cycles.SolverConfig`` for a batch of B right-hand sides."""
     from .mesh import HaloMode
 
@@ -51,7 +52,7 @@ def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
         mode, P = GEOM_HALO, 1
         b = sm.buffer if sm.buffer is not None else sm.halo_mode.halo
     return PlanKey(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns, mode, int(P), int(b),
-                   int(B), dtype, float(sm.omega), fused, use_graph)
+                   int(B), dtype, float(sm.omega), fused, use_graph, coarse)
 
 
 class FmgPlan:
@@ -66,6 +67,7 @@ class FmgPlan:
         d.omega = key.omega
         d.fused = int(key.fused)
         d.use_graph = int(key.use_graph)
+        d.coarse = int(key.coarse)
         h = C.c_void_p()
         N.check(N.lib().fmgsr_plan_create(C.byref(d), C.byref(h)), "plan_create")
         self._h = h
@@ -109,7 +111,7 @@ class FmgPlan:
         N.check(N.lib().fmgsr_plan_solve_timed(self._h, forcing.data_ptr(), out.data_ptr(),
                                                N.stream_ptr(), ms, lvl, kind, cap,
                                                C.byref(nv)), "plan_solve_timed")
-        names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade"}
+        names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade", 5: "coarse"}
         return [(names[kind[i]], lvl[i], ms[i]) for i in range(min(nv.value, cap))]
 
     def info(self) -> dict:
@@ -121,6 +123,8 @@ class FmgPlan:
             "visits_per_solve": inf.visits_per_solve,
             "alg_bytes_per_solve": inf.alg_bytes_per_solve,
             "finest_visit_alg_bytes": inf.finest_visit_alg_bytes,
+            "coarse_cutoff": inf.coarse_cutoff,
+            "coarse_columns": inf.coarse_columns,
         }
 
 

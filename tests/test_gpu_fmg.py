@@ -22,7 +22,8 @@ def config_from_params(fm, params):
     return fm.SolverConfig(hierarchy=fm.build_hierarchy(m0, m), n_sr=n_sr, smoother=sm)
 
 
-@pytest.mark.parametrize("path", ["plan_fused", "plan_unfused", "operators"])
+@pytest.mark.parametrize("path", ["plan_fused", "plan_fused_nocoarse", "plan_coarse_all",
+                                  "plan_unfused", "operators"])
 def test_fmg_matches_golden(fm, golden, path):
     for name in golden["fmg_cases"]:
         p = str(name) + "/"
@@ -30,6 +31,10 @@ def test_fmg_matches_golden(fm, golden, path):
         forcing = golden[p + "forcing"]
         if path == "operators":
             got, _ = fm.fmg_solve(cfg, forcing, keep_state=True)
+        elif path == "plan_fused_nocoarse":
+            got, _ = fm.fmg_solve(cfg, forcing, coarse=0)
+        elif path == "plan_coarse_all":  # every level but the finest on chip
+            got, _ = fm.fmg_solve(cfg, forcing, coarse=cfg.hierarchy.m)
         else:
             got, _ = fm.fmg_solve(cfg, forcing, fused=(path == "plan_fused"))
         assert np.array_equal(got, golden[p + "solution"]), (path, str(name))
@@ -69,12 +74,14 @@ def test_fmg_batch_matches_oracle(fm, oracle, m, P, b, n_sr, ns):
     cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
                           smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b))
     f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + P + b))
-    got = fm.fmg_solve(cfg, f)[0].cpu().numpy()
-    got_unfused = fm.fmg_solve(cfg, f, fused=False)[0].cpu().numpy()
     want = oracle.fmg_solve_batch(oracle_cfg(oracle, cfg), np.ascontiguousarray(f.cpu().numpy().T),
                                   nthreads=8).T
-    assert np.array_equal(got, want)
-    assert np.array_equal(got_unfused, want)
+    variants = {"auto": dict(), "unfused": dict(fused=False), "no_coarse": dict(coarse=0),
+                "coarse_m0": dict(coarse=4), "coarse_mid": dict(coarse=m - 3),
+                "coarse_all": dict(coarse=m)}
+    for name, kw in variants.items():
+        got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
+        assert np.array_equal(got, want), name
 
 
 def test_zero_forcing_gives_zero(fm):
