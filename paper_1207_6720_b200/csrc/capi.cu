@@ -8,6 +8,7 @@
 // and captures the whole cycle into a CUDA graph that is replayed per solve.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -88,6 +89,7 @@ struct Plan : PlanBase {
   // coarse hierarchy kernel: levels m0..Lc on chip, CW RHS columns per CTA
   bool use_coarse = false;
   int Lc = 0, CW = 1;
+  int coarse_trace = 0;
 
   bool is_sr(int l) const { return l > d.m - d.n_sr; }
 
@@ -148,6 +150,8 @@ struct Plan : PlanBase {
     // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
     // three fields per level (two u, f) for CW columns fit in ~200 KB.
     use_coarse = d.fused && d.ns == 1 && d.coarse != 0;
+    const char* tr = getenv("FMGSR_COARSE_TRACE");
+    coarse_trace = (tr && tr[0] == '1') ? 1 : 0;
     if (use_coarse) {
       i64 cw = 1;
       while (cw * 2 <= 32 && cw * 2 * 128 <= d.B) cw *= 2;
@@ -420,6 +424,7 @@ struct Plan : PlanBase {
     a.kz.proj_diag = (T)0.5;
     a.kz.recip = (T)2.0;
     a.kz.pow2 = true;
+    a.trace = coarse_trace;
     return a;
   }
 

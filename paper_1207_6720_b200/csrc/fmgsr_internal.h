@@ -77,6 +77,7 @@ struct CoarseArgs {
   T* u_top = nullptr;        // mode 1: in/out u_{Lc}; mode 0: out
   double omega = 1.0;
   KzCoef<T> kz{};
+  int trace = 0;  // debug: per-phase clock printf from CTA 0
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
 template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW);

@@ -17,6 +17,7 @@
 // The same launch also hosts the multi-level restriction of the forcing
 // (the f cascade, cycles.py:178-180).
 #include <cmath>
+#include <cstdio>
 
 #include "fmgsr_device.cuh"
 #include "fmgsr_internal.h"
@@ -27,9 +28,11 @@ namespace {
 
 constexpr int CNT = 512;  // threads per coarse CTA
 
+// 2^e built from its exponent bits (exact; no int -> fp conversion)
+__device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 template <typename T>
 __device__ __forceinline__ T pow4(int l) {
-  return (T)(double)((i64)1 << (2 * l));
+  return (T)pow2d(2 * l);
 }
 
 // Shared-memory layout of the coarse hierarchy for CW columns: level l keeps
@@ -58,11 +61,32 @@ struct CoarseCtx {
 
   __device__ bool sr(int l) const { return l > a.m - a.n_sr; }
 
+  // barrier between phases; FMGSR_COARSE_TRACE=1 makes CTA 0 printf the
+  // clock at every barrier (phase-latency profiling, off by default)
+  int nbar;
+  __device__ __forceinline__ long long* tstamp() const {
+    __shared__ long long ts[96];
+    return ts;
+  }
+  __device__ __forceinline__ void bar(const char* what, int l) {
+    __syncthreads();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < 96) tstamp()[nbar++] = clock64();
+  }
+  __device__ void dump() {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0)
+      for (int i = 1; i < nbar; i++)
+        printf("coarse-trace %d %lld\n", i, tstamp()[i] - tstamp()[i - 1]);
+  }
+
+  // global -> shared by cp.async: every element in flight at once, one wait
   __device__ void load(T* dst, const T* src, int n) {
     for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
       int i = e / CW, c = e % CW, col = c0 + c;
-      dst[e] = col < a.B ? src[(i64)i * a.ld + col] : T(0);
+      if (col < a.B) cp_async(dst + e, src + (i64)i * a.ld + col);
+      else dst[e] = T(0);
     }
+    cp_commit();
+    cp_wait<0>();
   }
   __device__ void store(T* dst, const T* src, int n) {
     for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
@@ -71,102 +95,111 @@ struct CoarseCtx {
     }
   }
 
-  // prolong_fmg, stencils.py:67-105: dst level l (nf cells) from src level l-1
-  __device__ void prolong(T* dst, const T* src, int nc) {
+  // ---- on-the-fly operators on one column (pointer already column-offset) ----
+  // prolong_fmg row i (stencils.py:67-105) from coarse column s of nc cells
+  __device__ __forceinline__ T fmg_row(const T* s, int i, int nc) const {
     const int nf = 2 * nc;
-    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x) {
-      int i = e / CW, c = e % CW;
-      const T* s = src + c;
 #define C(k) s[(k) * CW]
-      T v;
-      if (i >= 4 && i < nf - 4) {
-        if ((i & 1) == 0) {
-          int q = i / 2;
-          v = xsub(xadd(xadd(xmul(T(-5), C(q - 2)), xmul(T(35), C(q - 1))), xmul(T(105), C(q))),
-                   xmul(T(7), C(q + 1)));
-        } else {
-          int q = (i - 1) / 2;
-          v = xsub(xadd(xadd(xmul(T(-7), C(q - 1)), xmul(T(105), C(q))), xmul(T(35), C(q + 1))),
-                   xmul(T(5), C(q + 2)));
-        }
-      } else if (i == 0) v = xsub(xmul(T(70), C(0)), xmul(T(2), C(1)));
-      else if (i == 1) v = xsub(xadd(xmul(T(112), C(0)), xmul(T(35), C(1))), xmul(T(5), C(2)));
-      else if (i == 2) v = xsub(xadd(xmul(T(40), C(0)), xmul(T(105), C(1))), xmul(T(7), C(2)));
-      else if (i == 3)
-        v = xsub(xadd(xadd(xmul(T(-7), C(0)), xmul(T(105), C(1))), xmul(T(35), C(2))),
-                 xmul(T(5), C(3)));
-      else if (i == nf - 4)
-        v = xsub(xadd(xadd(xmul(T(-7), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(35), C(nc - 3))),
-                 xmul(T(5), C(nc - 4)));
-      else if (i == nf - 3)
-        v = xsub(xadd(xmul(T(40), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(7), C(nc - 3)));
-      else if (i == nf - 2)
-        v = xsub(xadd(xmul(T(112), C(nc - 1)), xmul(T(35), C(nc - 2))), xmul(T(5), C(nc - 3)));
-      else v = xsub(xmul(T(70), C(nc - 1)), xmul(T(2), C(nc - 2)));
-#undef C
-      dst[e] = xmul(v, T(0.0078125));
-    }
-  }
-
-  // cycles.py:120-121: dst = u + P(uH - R u), u on level with nf cells
-  __device__ void correct(T* dst, const T* u, const T* uH, int nf) {
-    const int nc = nf / 2;
-    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x) {
-      int i = e / CW, c = e % CW;
-      const T* ur = u + c;
-      const T* hr = uH + c;
-      auto cc = [&](int j) {
-        return xsub(hr[j * CW], xmul(T(0.5), xadd(ur[(2 * j) * CW], ur[(2 * j + 1) * CW])));
-      };
-      T p;
-      if (i == 0) p = xmul(T(0.5), cc(0));
-      else if (i == nf - 1) p = xmul(T(0.5), cc(nc - 1));
-      else if (i & 1) {
-        int j = (i - 1) / 2;
-        p = xmul(T(0.25), xadd(xmul(T(3), cc(j)), cc(j + 1)));
+    T v;
+    if (i >= 4 && i < nf - 4) {
+      if ((i & 1) == 0) {
+        int q = i >> 1;
+        v = xsub(xadd(xadd(xmul(T(-5), C(q - 2)), xmul(T(35), C(q - 1))), xmul(T(105), C(q))),
+                 xmul(T(7), C(q + 1)));
       } else {
-        int j = (i - 2) / 2;
-        p = xmul(T(0.25), xadd(cc(j), xmul(T(3), cc(j + 1))));
+        int q = i >> 1;
+        v = xsub(xadd(xadd(xmul(T(-7), C(q - 1)), xmul(T(105), C(q))), xmul(T(35), C(q + 1))),
+                 xmul(T(5), C(q + 2)));
       }
-      dst[e] = xadd(ur[i * CW], p);
-    }
+    } else if (i == 0) v = xsub(xmul(T(70), C(0)), xmul(T(2), C(1)));
+    else if (i == 1) v = xsub(xadd(xmul(T(112), C(0)), xmul(T(35), C(1))), xmul(T(5), C(2)));
+    else if (i == 2) v = xsub(xadd(xmul(T(40), C(0)), xmul(T(105), C(1))), xmul(T(7), C(2)));
+    else if (i == 3)
+      v = xsub(xadd(xadd(xmul(T(-7), C(0)), xmul(T(105), C(1))), xmul(T(35), C(2))), xmul(T(5), C(3)));
+    else if (i == nf - 4)
+      v = xsub(xadd(xadd(xmul(T(-7), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(35), C(nc - 3))),
+               xmul(T(5), C(nc - 4)));
+    else if (i == nf - 3)
+      v = xsub(xadd(xmul(T(40), C(nc - 1)), xmul(T(105), C(nc - 2))), xmul(T(7), C(nc - 3)));
+    else if (i == nf - 2)
+      v = xsub(xadd(xmul(T(112), C(nc - 1)), xmul(T(35), C(nc - 2))), xmul(T(5), C(nc - 3)));
+    else v = xsub(xmul(T(70), C(nc - 1)), xmul(T(2), C(nc - 2)));
+#undef C
+    return xmul(v, T(0.0078125));
   }
 
-  // restrict + coarse_rhs (stencils.py:39-47, 108-125), level l -> l-1
-  __device__ void restrict_tau(const T* u, const T* f, T* uH, T* fH, int nf, int l) {
-    const int nc = nf / 2;
+  // u[i] + P(uH - R u)[i] (cycles.py:120-121, stencils.py:39-64); u has nf cells
+  __device__ __forceinline__ T corr_row(const T* u, const T* uH, int i, int nf) const {
+    const int nc = nf >> 1;
+    auto cc = [&](int j) {
+      return xsub(uH[j * CW], xmul(T(0.5), xadd(u[(2 * j) * CW], u[(2 * j + 1) * CW])));
+    };
+    T p;
+    if (i == 0) p = xmul(T(0.5), cc(0));
+    else if (i == nf - 1) p = xmul(T(0.5), cc(nc - 1));
+    else if (i & 1) {
+      int j = (i - 1) >> 1;
+      p = xmul(T(0.25), xadd(xmul(T(3), cc(j)), cc(j + 1)));
+    } else {
+      int j = (i - 2) >> 1;
+      p = xmul(T(0.25), xadd(cc(j), xmul(T(3), cc(j + 1))));
+    }
+    return xadd(u[i * CW], p);
+  }
+
+  // coarse_rhs at coarse cell j (stencils.py:108-125) from fine u, f of nf
+  // cells on level lf (ih = 4^lf, iH = 4^(lf-1))
+  __device__ __forceinline__ T crhs_row(const T* u, const T* f, int j, int nf, T ih, T iH) const {
+    const int nc = nf >> 1;
+    auto ru = [&](int k) { return xmul(T(0.5), xadd(u[(2 * k) * CW], u[(2 * k + 1) * CW])); };
+    auto lu = [&](int i) {
+      T s;
+      if (i == 0) s = xsub(xmul(T(3), u[0]), u[CW]);
+      else if (i == nf - 1) s = xsub(xmul(T(3), u[(nf - 1) * CW]), u[(nf - 2) * CW]);
+      else s = xsub(xsub(xmul(T(2), u[i * CW]), u[(i - 1) * CW]), u[(i + 1) * CW]);
+      return xmul(s, ih);
+    };
+    T Rj = ru(j);
+    T LH;
+    if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru(1)), iH);
+    else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rj), ru(nc - 2)), iH);
+    else LH = xmul(xsub(xsub(xmul(T(2), Rj), ru(j - 1)), ru(j + 1)), iH);
+    T RL = xmul(T(0.5), xadd(lu(2 * j), lu(2 * j + 1)));
+    T Rf = xmul(T(0.5), xadd(f[(2 * j) * CW], f[(2 * j + 1) * CW]));
+    return xadd(Rf, xsub(LH, RL));
+  }
+
+  // ---- data-parallel stencil phases (one thread per output element) ---------------
+  __device__ void phase_fmg(T* dst, const T* uH, int l) {  // dst = Pi uH (level l)
+    const int nf = nlev(l);
+    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x)
+      dst[e] = fmg_row(uH + e % CW, e / CW, nf >> 1);
+  }
+  __device__ void phase_corr(T* dst, const T* u, const T* uH, int l) {  // u + P(uH - R u)
+    const int nf = nlev(l);
+    for (int e = threadIdx.x; e < nf * CW; e += blockDim.x)
+      dst[e] = corr_row(u + e % CW, uH + e % CW, e / CW, nf);
+  }
+  __device__ void phase_restrict(T* uH, T* fH, const T* u, const T* f, int l) {  // level l -> l-1
+    const int nf = nlev(l), nc = nf >> 1;
     const T ih = pow4<T>(l), iH = pow4<T>(l - 1);
     for (int e = threadIdx.x; e < nc * CW; e += blockDim.x) {
-      int j = e / CW, c = e % CW;
-      const T* ur = u + c;
-      auto ru = [&](int k) { return xmul(T(0.5), xadd(ur[(2 * k) * CW], ur[(2 * k + 1) * CW])); };
-      auto lu = [&](int i) {
-        T s;
-        if (i == 0) s = xsub(xmul(T(3), ur[0]), ur[CW]);
-        else if (i == nf - 1) s = xsub(xmul(T(3), ur[(nf - 1) * CW]), ur[(nf - 2) * CW]);
-        else s = xsub(xsub(xmul(T(2), ur[i * CW]), ur[(i - 1) * CW]), ur[(i + 1) * CW]);
-        return xmul(s, ih);
-      };
-      T Rj = ru(j);
-      T LH;
-      if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru(1)), iH);
-      else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rj), ru(nc - 2)), iH);
-      else LH = xmul(xsub(xsub(xmul(T(2), Rj), ru(j - 1)), ru(j + 1)), iH);
-      T RL = xmul(T(0.5), xadd(lu(2 * j), lu(2 * j + 1)));
-      T Rf = xmul(T(0.5), xadd(f[(2 * j) * CW + c], f[(2 * j + 1) * CW + c]));
-      fH[e] = xadd(Rf, xsub(LH, RL));
-      uH[e] = Rj;
+      const int j = e / CW, c = e % CW;
+      fH[e] = crhs_row(u + c, f + c, j, nf, ih, iH);
+      uH[e] = xmul(T(0.5), xadd(u[(2 * j) * CW + c], u[(2 * j + 1) * CW + c]));
     }
   }
 
-  // additive patch smoother, ns = 1 (_kernels_numba.py:60-92), one chain per
-  // (patch, column); Kaczmarz applied per cell from the unmodified input
-  __device__ void smooth(int l, const T* uin, const T* f, const T* uc, T* out) {
+  // ---- patch chains: additive ns = 1 smoother (_kernels_numba.py:60-92) -----------
+  // one chain per (patch, column) over the precomputed input uin; Kaczmarz (CR)
+  // per pair inside the window; domain-boundary rows peeled off the loop.
+  template <bool CR>
+  __device__ void chains(int l, const T* uin, const T* f, const T* uc, T* out) {
     const int n = nlev(l), W = (int)a.W[l], b = (int)a.b[l];
     const int P = n / W;
     GsCoef<T> gc;
     gc.inv_h2 = pow4<T>(l);
-    gc.rdiag = (T)(1.0 / (2.0 * (double)((i64)1 << (2 * l))));
+    gc.rdiag = (T)pow2d(-(2 * l + 1));
     gc.diag_b = xmul(T(3), gc.inv_h2);
     gc.omega = (T)a.omega;
     for (int k = threadIdx.x; k < P * CW; k += blockDim.x) {
@@ -179,34 +212,45 @@ struct CoarseCtx {
       const T* fc = f + c;
       T* oc = out + c;
       auto val = [&](int x) -> T {
+        if (!CR) return ui[x * CW];
+        const int j = x >> 1;
         T v = ui[x * CW];
-        if (uc) {
-          int j = x >> 1;
-          if (j >= wlo && j < whi) {
-            T aa = ui[(2 * j) * CW], bb = ui[(2 * j + 1) * CW];
-            kaczmarz_pair(aa, bb, uc[j * CW + c], a.kz);
-            v = (x & 1) ? bb : aa;
-          }
+        if (j >= wlo && j < whi) {
+          T aa = ui[(2 * j) * CW], bb = ui[(2 * j + 1) * CW];
+          kaczmarz_pair(aa, bb, uc[j * CW + c], a.kz);
+          v = (x & 1) ? bb : aa;
         }
         return v;
       };
+      int i = ws;
       T uL = ws > 0 ? val(ws - 1) : T(0);
       T cu = val(ws);
-      T nx = (ws + 1 < n) ? val(ws + 1) : T(0);
-      for (int i = ws; i < oe; i++) {
-        T nn = (i + 2 < n) ? val(i + 2) : T(0);  // one cell of lookahead beyond nx
-        T v = gs_cell(gc, (i64)i, (i64)n, uL, cu, nx, fc[i * CW]);
+      T nx = val(ws + 1);  // n >= 8 on every smoothed level
+      if (i == 0) {
+        T v = gs_bnd(gc, cu, nx, fc[0]);
+        if (os == 0) oc[0] = v;
+        uL = v;
+        cu = nx;
+        nx = val(2);
+        i = 1;
+      }
+      const int iend = oe < n - 1 ? oe : n - 1;
+      for (; i < iend; i++) {
+        T nn = val(i + 2 < n ? i + 2 : n - 1);
+        T v = gs_int(gc, uL, cu, nx, fc[i * CW]);
         if (i >= os) oc[i * CW] = v;
         uL = v;
         cu = nx;
         nx = nn;
       }
+      if (oe == n) oc[(n - 1) * CW] = gs_bnd(gc, cu, uL, fc[(n - 1) * CW]);
     }
   }
 
   // LAPACK ?ptsv order (smoothers.py:210-225): dptts2 with the shared factor
-  __device__ void direct(const T* f, T* u) {
+  __device__ void direct(T* u) {
     const int n = nlev(a.m0);
+    const T* f = Fl(a.m0);
     for (int c = threadIdx.x; c < CW; c += blockDim.x) {
       T prev = f[c];
       u[c] = prev;
@@ -223,43 +267,44 @@ struct CoarseCtx {
     }
   }
 
-  // ---- level visits (each ends with a barrier) ---------------------------------
+  // ---- level visits (each phase ends with a barrier) ----------------------------
   __device__ void visit_top(int t) {  // Pi, pre-smooth, restrict + tau
-    int h = cur(t - 1);
-    prolong(U(t, 1), U(t - 1, h), nlev(t - 1));
-    __syncthreads();
-    smooth(t, U(t, 1), Fl(t), nullptr, U(t, 0));
+    const int h = cur(t - 1);
+    phase_fmg(U(t, 1), U(t - 1, h), t);
+    bar("T.fmg", t);
+    chains<false>(t, U(t, 1), Fl(t), nullptr, U(t, 0));
     set0(t);
-    __syncthreads();
-    restrict_tau(U(t, 0), Fl(t), U(t - 1, h ^ 1), Fl(t - 1), nlev(t), t);
+    bar("T.smooth", t);
+    phase_restrict(U(t - 1, h ^ 1), Fl(t - 1), U(t, 0), Fl(t), t);
     flip(t - 1);
-    __syncthreads();
+    bar("T.restrict", t);
   }
   __device__ void visit_down(int l) {
-    int c = cur(l);
-    smooth(l, U(l, c), Fl(l), nullptr, U(l, c ^ 1));
+    const int c = cur(l);
+    chains<false>(l, U(l, c), Fl(l), nullptr, U(l, c ^ 1));
     flip(l);
-    __syncthreads();
-    int h = cur(l - 1);
-    restrict_tau(U(l, c ^ 1), Fl(l), U(l - 1, h ^ 1), Fl(l - 1), nlev(l), l);
+    bar("D.smooth", l);
+    const int h = cur(l - 1);
+    phase_restrict(U(l - 1, h ^ 1), Fl(l - 1), U(l, c ^ 1), Fl(l), l);
     flip(l - 1);
-    __syncthreads();
+    bar("D.restrict", l);
   }
   __device__ void visit_direct() {
-    int c = cur(a.m0);
-    direct(Fl(a.m0), U(a.m0, c ^ 1));
+    const int c = cur(a.m0);
+    direct(U(a.m0, c ^ 1));
     flip(a.m0);
-    __syncthreads();
+    bar("direct", a.m0);
   }
   __device__ void visit_up(int l) {
-    int c = cur(l);
+    const int c = cur(l);
     const T* uH = U(l - 1, cur(l - 1));
     const bool s = sr(l);
-    if (s) prolong(U(l, c ^ 1), uH, nlev(l - 1));
-    else correct(U(l, c ^ 1), U(l, c), uH, nlev(l));
-    __syncthreads();
-    smooth(l, U(l, c ^ 1), Fl(l), s ? uH : nullptr, U(l, c));
-    __syncthreads();
+    if (s) phase_fmg(U(l, c ^ 1), uH, l);
+    else phase_corr(U(l, c ^ 1), U(l, c), uH, l);
+    bar("U.prolong", l);
+    if (s) chains<true>(l, U(l, c ^ 1), Fl(l), uH, U(l, c));
+    else chains<false>(l, U(l, c ^ 1), Fl(l), nullptr, U(l, c));
+    bar("U.smooth", l);
   }
 };
 
@@ -270,6 +315,8 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
   x.sm = reinterpret_cast<T*>(coarse_smem);
   x.c0 = blockIdx.x * CW;
   x.curmask = 0;
+  x.nbar = 0;
+  x.bar("start", 0);
   const int m0 = a.m0, Lc = a.Lc;
   const int n0 = 1 << m0;
   T* d = x.sm + 3 * CW * ((1 << (Lc + 1)) - (1 << m0));
@@ -290,11 +337,11 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
   x.efac = e;
   if (a.mode == 0) {
     x.load(x.Fl(m0), a.forig[m0], n0);
-    __syncthreads();
+    x.bar("load", m0);
     x.visit_direct();
     for (int t = m0 + 1; t <= Lc; t++) {
       x.load(x.Fl(t), a.forig[t], 1 << t);
-      __syncthreads();
+      x.bar("load", t);
       x.visit_top(t);
       for (int l = t - 1; l > m0; l--) x.visit_down(l);
       x.visit_direct();
@@ -303,12 +350,14 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
   } else {
     x.load(x.U(Lc, 0), a.u_top, 1 << Lc);
     x.load(x.Fl(Lc), a.f_top, 1 << Lc);
-    __syncthreads();
+    x.bar("load", Lc);
     for (int l = Lc; l > m0; l--) x.visit_down(l);
     x.visit_direct();
     for (int l = m0 + 1; l <= Lc; l++) x.visit_up(l);
   }
   x.store(a.u_top, x.U(Lc, x.cur(Lc)), 1 << Lc);
+  x.bar("store", Lc);
+  x.dump();
 }
 
 // f cascade: each thread restricts 2^S consecutive rows of one column down S
@@ -352,13 +401,20 @@ size_t coarse_smem_bytes(int m0, int Lc, int CW) {
 
 template <typename T, int CW>
 static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static int granted = -1;  // dynamic smem opted in for this instantiation
+  if (granted < 0) {
+    int dev = 0, optin = 0;
+    check_cuda(cudaGetDevice(&dev), "coarse device");
+    check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
+               "coarse smem optin");
+    cudaFuncAttributes fa;
+    check_cuda(cudaFuncGetAttributes(&fa, coarse_kernel<T, CW>), "coarse attrs");
+    granted = optin - (int)fa.sharedSizeBytes;
     check_cuda(cudaFuncSetAttribute(coarse_kernel<T, CW>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, granted),
                "coarse smem attr");
-    attr = true;
   }
+  require(smem <= (size_t)granted, "coarse: shared memory budget exceeded");
   unsigned blocks = (unsigned)((a.B + CW - 1) / CW);
   coarse_kernel<T, CW><<<blocks, CNT, smem, s>>>(a);
 }
