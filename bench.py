@@ -37,6 +37,28 @@ METRIC = "fine-grid unknowns solved/sec (one FMG-FAS-SR cycle)"
 UNIT = "unknowns/s"
 
 
+def throughput(world: int, B: int, n: int, ms_step: float) -> float:
+    """Whole-job fine-grid unknowns per second: every rank solves B RHS of n cells."""
+    return world * B * n / (ms_step / 1e3)
+
+
+def reduce_max(x: float, world: int, device: str = "cuda") -> float:
+    """Max over ranks (the step time the job is charged with)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def rank_seed(rank: int) -> int:
+    """Seed of the rank's RHS batch: independent problems per rank."""
+    return 1000 * rank
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,7 +224,7 @@ def run_gpu(args, w):
     cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], m), n_sr=w["n_sr"],
                           smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
     plan = fm.get_plan(fm.key_from_config(cfg, B, dtype))
-    coef = fm.fourier_coefficients(B, seed=1000 * rank)
+    coef = fm.fourier_coefficients(B, seed=rank_seed(rank))
     f, _ = fm.fourier_batch(n, coef, dtype, with_exact=False)
     sol = torch.empty_like(f)
     stream = torch.cuda.current_stream()
@@ -229,13 +251,9 @@ def run_gpu(args, w):
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = reduce_max(e0.elapsed_time(e1), world)
     ms_step = ms_max / args.steps
-    value = world * B * n / (ms_step / 1e3)
+    value = throughput(world, B, n, ms_step)
 
     # ---- end to end through the public API with host buffers ----------------------
     hf = f.cpu().pin_memory()
@@ -258,11 +276,8 @@ def run_gpu(args, w):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item()) / args.steps
-    e2e_val = world * B * n / (e2e_ms / 1e3)
+    e2e_ms = reduce_max(e0.elapsed_time(e1), world) / args.steps
+    e2e_val = throughput(world, B, n, e2e_ms)
     nbytes = n * B * (8 if dtype == torch.float64 else 4)
 
     # ---- per-visit kernel times (CUDA events on the launching stream) -------------
