@@ -18,9 +18,13 @@
 
 #include "fmgsr_device.cuh"
 
+#ifndef FMGSR_PROXY_FENCE
+#define FMGSR_PROXY_FENCE 0
+#endif
+
 namespace fmgsr {
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D>
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D, bool BULK>
 struct Chain {
   static constexpr int R = SrcRows<SRC, CR>::R;
   PairSource<T, SRC, CR> src;
@@ -30,10 +34,43 @@ struct Chain {
   bool store;
   T* ring;  // this lane's ring: slot s, row k at ring[(s * R + k) * NT]
   Epilogue<T>* epi;
+  // BULK staging: the warp's D mbarriers; pair x lives in slot x & (D-1) and
+  // completes phase ((x - x0) / D) & 1 of that slot's barrier
+  unsigned long long* bars;
+  int lane;
+  i64 x0;
   // chain state: uL = new value left of the current pair; (v0, v1, f0, f1) = current pair
   T uL, v0, v1, f0, f1;
 
   __device__ __forceinline__ T* slot(i64 x) const { return ring + (i64)((x & (D - 1)) * R) * NT; }
+
+  // stage pair g into slot(g): per-lane cp.async, or one bulk copy per row
+  __device__ __forceinline__ void stage(i64 g) {
+    if (!BULK) {
+      src.template issue<NT>(slot(g), g);
+      cp_commit();
+      return;
+    }
+    __syncwarp();  // every lane is done reading this slot's previous pair
+    if (lane == 0) {
+      const T* p[R];
+      src.rows(g, 0, p);
+      unsigned long long* bar = bars + (g & (D - 1));
+      T* dst = slot(g);  // lane 0: the warp's 32-column segment of each row
+      if (FMGSR_PROXY_FENCE) fence_proxy_async();
+      mbar_expect_tx(bar, R * 32 * sizeof(T));
+#pragma unroll
+      for (int k = 0; k < R; k++) bulk_g2s(dst + k * NT, p[k], 32 * sizeof(T), bar);
+    }
+  }
+  // wait until pair g has landed in its slot
+  __device__ __forceinline__ void await(i64 g) {
+    if (!BULK) {
+      cp_wait<D - 2>();
+      return;
+    }
+    mbar_wait(bars + (g & (D - 1)), (unsigned)(((g - x0) / D) & 1));
+  }
 
   __device__ __forceinline__ T gsi(T l, T u, T r, T f) const {
     T s = xsub(xsub(xmul(T(2), u), l), r);
@@ -44,10 +81,9 @@ struct Chain {
 
   // general step for pair q (every boundary case, exactly as the reference)
   __device__ __forceinline__ void step_slow(i64 q) {
-    cp_wait<D - 2>();
+    await(q + 1);
     Raw<T> r = src.template fetch<NT>(slot(q + 1));
-    src.template issue<NT>(slot(q), q + D);
-    cp_commit();
+    stage(q + D);
     T w0, w1;
     src.make(q + 1, r, w0, w1);
     const i64 i0 = 2 * q, i1 = i0 + 1;
@@ -85,16 +121,20 @@ struct Chain {
   // interior pairs [q, q_end]: OWNED selects store/epilogue
   template <bool OWNED>
   __device__ __forceinline__ void run_fast(i64 q, i64 q_end) {
-    src.fast_ptrs(q + D);
+    if (!BULK) src.fast_ptrs(q + D);
     T* po = (OWNED && out) ? out + (2 * q) * ld : nullptr;
     if (EPI && OWNED) epi->fast_begin(q);
     const bool st_u = OWNED && out && store;
 #pragma unroll 2
     for (; q <= q_end; q++) {
-      cp_wait<D - 2>();
+      await(q + 1);
       Raw<T> r = src.template fetch<NT>(slot(q + 1));
-      src.template issue_fast<NT>(slot(q));
-      cp_commit();
+      if (BULK) {
+        stage(q + D);
+      } else {
+        src.template issue_fast<NT>(slot(q));
+        cp_commit();
+      }
       T w0, w1;
       src.make_fast(r, w0, w1);
       T n0 = gsi(uL, v0, v1, f0);
@@ -126,10 +166,8 @@ struct Chain {
       f0 = r.f0;
       f1 = r.f1;
     }
-    for (int k = 1; k < D; k++) {
-      src.template issue<NT>(slot(qs + k), qs + k);
-      cp_commit();
-    }
+    x0 = qs + 1;
+    for (int k = 1; k < D; k++) stage(qs + k);
     uL = T(0);
     // interior range: both cells updated and interior, generation of q+1
     // interior, CR window interior, unclamped fast issue of q + D
@@ -162,7 +200,12 @@ struct Chain {
       q = hi + 1;
     }
     for (; q <= qe; q++) step_slow(q);
-    cp_wait<0>();
+    if (BULK) {
+      // drain the pairs still in flight before the CTA may exit
+      for (i64 g = qe + 2; g <= qe + D; g++) await(g);
+    } else {
+      cp_wait<0>();
+    }
   }
 };
 

@@ -103,6 +103,46 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// 1D bulk copies (TMA engine, cp.async.bulk) completing on an mbarrier: one
+// lane moves a whole 32-column row segment per instruction.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 // ---------------------------------------------------------------------------
 // Pair sources: produce the smoother input u_in at fine cells (2q, 2q+1)
 // together with f there, streaming in increasing q.
@@ -166,6 +206,26 @@ struct PairSource {
       cp_async(sl + 2 * NT, uH + cl(g + 2) * ld);
     }
     if (CR && SRC != SRC_FMG) cp_async(sl + (R - 1) * NT, uc + gg * ld);
+  }
+
+  // the R source rows of pair g (clamped), per-lane pointers shifted by -off
+  // (off = lane gives the warp's 32-column row segment for a bulk copy)
+  __device__ __forceinline__ void rows(i64 g, int off, const T* (&p)[R]) const {
+    i64 gg = cl(g);
+    p[0] = f + (2 * gg) * ld - off;
+    p[1] = f + (2 * gg + 1) * ld - off;
+    if (SRC == SRC_LOAD) {
+      p[2] = u + (2 * gg) * ld - off;
+      p[3] = u + (2 * gg + 1) * ld - off;
+    } else if (SRC == SRC_CORR) {
+      i64 g1 = cl(g + 1);
+      p[2] = u + (2 * g1) * ld - off;
+      p[3] = u + (2 * g1 + 1) * ld - off;
+      p[4] = uH + g1 * ld - off;
+    } else {
+      p[2] = uH + cl(g + 2) * ld - off;
+    }
+    if (CR && SRC != SRC_FMG) p[R - 1] = uc + gg * ld - off;
   }
 
   __device__ __forceinline__ void fast_ptrs(i64 g) {

@@ -11,6 +11,8 @@
 // a global scratch and replayed exactly as the reference does (Kaczmarz
 // pass, GS pass, direction flip per repetition, owned write-back).
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "fmgsr_chain.cuh"
 #include "fmgsr_internal.h"
@@ -35,13 +37,17 @@ constexpr int VNT = 128;  // threads per block of the visit kernel
 constexpr int VD = 8;     // cp.async ring depth (pairs) per lane
 
 template <typename T, int SRC, bool CR>
-constexpr size_t visit_smem_bytes() {
+__host__ __device__ constexpr size_t visit_ring_bytes() {
   return (size_t)VD * SrcRows<SRC, CR>::R * VNT * sizeof(T);
 }
+template <typename T, int SRC, bool CR>
+__host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one mbarrier per (warp, slot)
+  return visit_ring_bytes<T, SRC, CR>() + (size_t)(VNT / 32) * VD * 8;
+}
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1>
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK>
 __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char visit_smem[];
+  extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 p = gw / a.nrg;
@@ -64,7 +70,16 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
     we = oe + a.b < a.n ? oe + a.b : a.n;
   }
 
-  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD> ch;
+  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD, BULK> ch;
+  ch.lane = lane;
+  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR>()) +
+            (threadIdx.x >> 5) * VD;
+  if (BULK) {
+    if (lane == 0)
+      for (int k = 0; k < VD; k++) mbar_init(ch.bars + k, 1);
+    mbar_fence_init();
+    __syncwarp();
+  }
   ch.src.u = a.u_src ? a.u_src + rr : nullptr;
   ch.src.uH = a.uH ? a.uH + rr : nullptr;
   ch.src.uc = a.uc ? a.uc + rr : nullptr;
@@ -126,6 +141,16 @@ static GsCoef<T> make_coef(i64 n, double omega) {
   return g;
 }
 
+// FMGSR_VISIT_STAGING=cpasync forces the per-lane cp.async staging (A/B tests)
+static bool visit_bulk_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FMGSR_VISIT_STAGING");
+    v = (e && std::string(e) == "cpasync") ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename T>
 static KzCoef<T> make_kz(double pd) {
   KzCoef<T> k;
@@ -136,28 +161,43 @@ static KzCoef<T> make_kz(double pd) {
   return k;
 }
 
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK>
+static void launch_visit_k(const VisitArgs<T>& a, i64 blocks, cudaStream_t s) {
+  constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
+  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK>;
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+    attr = true;
+  }
+  k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+}
+
+// Bulk (TMA) staging needs whole 32-column row segments at 16-byte alignment.
+template <typename T>
+static bool bulk_ok(const VisitArgs<T>& a) {
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  return a.B % 32 == 0 && (a.ld * sizeof(T)) % 16 == 0 && al(a.f) &&
+         (!a.u_src || al(a.u_src)) && (!a.uH || al(a.uH)) && (!a.uc || al(a.uc)) &&
+         visit_bulk_enabled();
+}
+
 template <typename T, int SRC, bool CR, bool EPI>
 static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   i64 warps = a.P * a.nrg;
   i64 blocks = (warps + VNT / 32 - 1) / (VNT / 32);
-  constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
   const bool om1 = a.gc.omega == T(1);
+  // bulk (TMA) staging pays off where per-lane LDGSTS saturates the MIO
+  // queue: sources with >= 5 staged rows per pair (the FAS-correction visits);
+  // measured slower than cp.async for 3-4 rows (profiles/r01 notes)
+  const bool bulk = SrcRows<SRC, CR>::R >= 5 && bulk_ok(a);
   if (om1) {
-    auto k = visit_kernel<T, SRC, CR, EPI, true>;
-    static bool attr = false;
-    if (!attr && smem > 48 * 1024) {
-      check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      attr = true;
-    }
-    k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+    if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true>(a, blocks, s);
+    else launch_visit_k<T, SRC, CR, EPI, true, false>(a, blocks, s);
   } else {
-    auto k = visit_kernel<T, SRC, CR, EPI, false>;
-    static bool attr = false;
-    if (!attr && smem > 48 * 1024) {
-      check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
-      attr = true;
-    }
-    k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+    if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true>(a, blocks, s);
+    else launch_visit_k<T, SRC, CR, EPI, false, false>(a, blocks, s);
   }
 }
 
