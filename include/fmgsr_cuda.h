@@ -162,6 +162,15 @@ int fmgsr_plan_destroy(void* plan);
 int fmgsr_plan_get_info(void* plan, fmgsr_plan_info* info);
 /* One FMG-FAS(-SR) solve of B RHS: forcing, solution are DEVICE [2^m][ld]. */
 int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stream);
+/* Host-buffer solve (the end-to-end entry point): HOST arrays [2^m][ld_host]
+ * holding chunks * B right-hand sides (B = the plan's batch, built with
+ * ld == B; page-locked memory for asynchronous copies).  Chunks are pipelined:
+ * H2D of chunk i+1, the solve of chunk i and D2H of chunk i-1 overlap on
+ * separate streams.  Ordered after prior work on `stream`; the results are in
+ * h_solution once `stream` reaches this point.  Two device buffer sets are
+ * allocated on the first call. */
+int fmgsr_plan_solve_host(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
+                          int64_t chunks, void* stream);
 /* Same solve launched op by op (no graph) with per-visit CUDA events for
  * profiling: writes up to `cap` visit durations (ms) and their levels. */
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

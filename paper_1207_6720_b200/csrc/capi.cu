@@ -58,6 +58,8 @@ struct PlanBase {
   virtual void solve_timed(const void* in, void* out, cudaStream_t s, float* ms, int32_t* lvl,
                            int32_t* kind, i64 cap, i64* nv) = 0;
   virtual void info(fmgsr_plan_info* inf) = 0;
+  virtual void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
+                          cudaStream_t s) = 0;
 };
 
 template <typename T>
@@ -154,19 +156,82 @@ struct Plan : PlanBase {
     coarse_trace = (tr && tr[0] == '1') ? 1 : 0;
     if (use_coarse) {
       i64 cw = 1;
-      while (cw * 2 <= 32 && cw * 2 * 128 <= d.B) cw *= 2;
+      // ~128 CTAs (one wave on 148 SMs); measured best against 256 / 512
+      i64 target = 128;
+      if (const char* e = getenv("FMGSR_COARSE_CTAS")) target = atoll(e);
+      while (cw * 2 <= 32 && cw * 2 * target <= d.B) cw *= 2;
       CW = (int)cw;
       Lc = m0;
       while (Lc + 1 <= m - 1 && coarse_smem_bytes<T>(m0, Lc + 1, CW) <= 200 * 1024) Lc++;
-      if (d.coarse > 0 && d.coarse - 1 >= m0 && d.coarse - 1 < Lc) Lc = d.coarse - 1;
+      int want = d.coarse;
+      if (want < 0)
+        if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
+      if (want > 0 && want - 1 >= m0 && want - 1 < Lc) Lc = want - 1;
     }
   }
 
   ~Plan() override {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : hev) cudaEventDestroy(e);
     if (cap) cudaStreamDestroy(cap);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     for (void* p : allocs) cudaFree(p);
+  }
+
+  // ---- host-buffer solve: chunks of B columns pipelined over PCIe ---------------
+  // Host arrays are [N][ld_host] with chunks * B columns.  Chunk i is copied
+  // (one cudaMemcpy2DAsync) into device buffer set i % 2 on s_in, solved on the
+  // caller's stream by the plan's graph for that buffer set, and copied back on
+  // s_out, so H2D of chunk i+1, the solve of chunk i and D2H of chunk i-1
+  // overlap.  The two buffer sets are allocated on first use.
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  T* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [set][forcing, solution]
+  std::vector<cudaEvent_t> hev;  // in_done[2], solved[2], out_done[2]
+
+  void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
+                  cudaStream_t s) override {
+    const i64 N = (i64)1 << d.m, B = d.B;
+    require(d.ld == B, "solve_host: the plan must be built with ld == B (one chunk)");
+    require(chunks >= 1 && ld_host >= chunks * B, "solve_host: ld_host < chunks * B");
+    if (!s_in) {
+      check_cuda(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "h2d stream");
+      check_cuda(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "d2h stream");
+      for (int k = 0; k < 2; k++)
+        for (int j = 0; j < 2; j++) hbuf[k][j] = alloc((size_t)N * B * sizeof(T));
+      hev.resize(6);
+      for (auto& e : hev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ev");
+    }
+    cudaEvent_t *in_done = &hev[0], *solved = &hev[2], *out_done = &hev[4];
+    const size_t row = (size_t)B * sizeof(T), pitch = (size_t)ld_host * sizeof(T);
+    // the caller's stream orders us after its prior work
+    for (int k = 0; k < 2; k++) {
+      check_cuda(cudaEventRecord(solved[k], s), "ev");
+      check_cuda(cudaEventRecord(out_done[k], s), "ev");
+    }
+    for (i64 i = 0; i < chunks; i++) {
+      const int k = (int)(i & 1);
+      const char* src = (const char*)h_in + i * row;
+      char* dst = (char*)h_out + i * row;
+      // H2D of chunk i once the solve of chunk i-2 no longer reads forcing set k
+      check_cuda(cudaStreamWaitEvent(s_in, solved[k], 0), "wait");
+      check_cuda(cudaMemcpy2DAsync(hbuf[k][0], row, src, pitch, row, N, cudaMemcpyHostToDevice,
+                                   s_in),
+                 "h2d");
+      check_cuda(cudaEventRecord(in_done[k], s_in), "ev");
+      // solve once the input landed and the D2H of chunk i-2 drained solution set k
+      check_cuda(cudaStreamWaitEvent(s, in_done[k], 0), "wait");
+      check_cuda(cudaStreamWaitEvent(s, out_done[k], 0), "wait");
+      solve(hbuf[k][0], hbuf[k][1], s);
+      check_cuda(cudaEventRecord(solved[k], s), "ev");
+      check_cuda(cudaStreamWaitEvent(s_out, solved[k], 0), "wait");
+      check_cuda(cudaMemcpy2DAsync(dst, pitch, hbuf[k][1], row, row, N, cudaMemcpyDeviceToHost,
+                                   s_out),
+                 "d2h");
+      check_cuda(cudaEventRecord(out_done[k], s_out), "ev");
+    }
+    for (int k = 0; k < 2; k++) check_cuda(cudaStreamWaitEvent(s, out_done[k], 0), "wait");
   }
 
   // ---- visit emitters ---------------------------------------------------
@@ -788,6 +853,14 @@ int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stre
     require(plan && forcing && solution, "plan_solve: null argument");
     require(forcing != solution, "plan_solve: solution must not alias forcing");
     reinterpret_cast<PlanBase*>(plan)->solve(forcing, solution, S(stream));
+  });
+}
+int fmgsr_plan_solve_host(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
+                          int64_t chunks, void* stream) {
+  return guarded([&] {
+    require(plan && h_forcing && h_solution, "plan_solve_host: null argument");
+    reinterpret_cast<PlanBase*>(plan)->solve_host(h_forcing, h_solution, ld_host, chunks,
+                                                  S(stream));
   });
 }
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

@@ -99,6 +99,22 @@ class FmgPlan:
                                          N.stream_ptr()), "plan_solve")
         return out
 
+    def solve_host(self, forcing: torch.Tensor, out: torch.Tensor, chunks: int) -> torch.Tensor:
+        """End-to-end solve from HOST memory: ``forcing`` / ``out`` are pinned CPU
+        tensors of shape (2**m, chunks * B); chunks of B right-hand sides are
+        pipelined H2D / solve / D2H on separate streams.  Returns ``out`` once
+        the current stream has reached the end of the pipeline."""
+        k = self.key
+        for name, t in (("forcing", forcing), ("solution", out)):
+            if t.is_cuda or t.dtype != k.dtype or tuple(t.shape) != (self.N, chunks * k.B) \
+                    or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous host {k.dtype} tensor of shape "
+                                 f"({self.N}, {chunks * k.B})")
+        N.check(N.lib().fmgsr_plan_solve_host(self._h, forcing.data_ptr(), out.data_ptr(),
+                                              chunks * k.B, chunks, N.stream_ptr()),
+                "plan_solve_host")
+        return out
+
     def solve_timed(self, forcing: torch.Tensor, out: torch.Tensor):
         """Launch op by op with CUDA events per level visit; returns
         [(kind, level, ms)] with kind in top/down/up/direct."""
