@@ -32,6 +32,8 @@ WORKLOADS = {
     "config4": dict(m0=3, m=24, P=4096, b=8, ns=1, n_sr=1, B=64, dtype="f64"),
     "config5": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f64"),
     "config5_f32": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f32"),
+    # BASELINE config 3: -u'' + u^3 = f, V(2,2), manufactured RHS scaled per RHS
+    "config3": dict(m0=3, m=20, P=256, b=4, ns=2, n_sr=1, B=256, dtype="f64", nonlinear=True),
 }
 METRIC = "fine-grid unknowns solved/sec (one FMG-FAS-SR cycle)"
 UNIT = "unknowns/s"
@@ -75,7 +77,8 @@ def cpu_rate(w, budget_s: float, nthreads: int, seed: int = 1):
     from oracle import oracle as O
 
     n = 2 ** w["m"]
-    cfg = O.make_cfg(w["m0"], w["m"], w["n_sr"], w["ns"], O.GEOM_PATCHES, w["P"], w["b"])
+    cfg = O.make_cfg(w["m0"], w["m"], w["n_sr"], w["ns"], O.GEOM_PATCHES, w["P"], w["b"],
+                     nonlin=bool(w.get("nonlinear", False)))
     x = (np.arange(n) + 0.5) / n
 
     def rhs(k):
@@ -130,7 +133,8 @@ def run_reference(args, w):
 
 def workload_config(name, w, world):
     return {
-        "workload": f"{name}: 1D Poisson FMG-FAS-SR, N=2^{w['m']} fine cells, m0={w['m0']}, "
+        "workload": f"{name}: 1D {'-u\'\'+u^3=f' if w.get('nonlinear') else 'Poisson'} "
+                    f"FMG-FAS-SR, N=2^{w['m']} fine cells, m0={w['m0']}, "
                     f"{w['P']} patches, {w['b']}-cell buffer, V({w['ns']},{w['ns']}), "
                     f"n_sr={w['n_sr']}, batch {w['B']} seeded Fourier RHS per GPU",
         "N": 2 ** w["m"], "batch_per_gpu": w["B"], "global_batch": w["B"] * world,
@@ -231,11 +235,16 @@ def run_gpu(args, w):
     dtype = torch.float64 if w["dtype"] == "f64" else torch.float32
     m, B = w["m"], w["B"]
     n = 2 ** m
+    nl = bool(w.get("nonlinear", False))
     cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], m), n_sr=w["n_sr"],
-                          smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+                          smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
+                                                     nonlinear=nl))
     plan = fm.get_plan(fm.key_from_config(cfg, B, dtype))
-    coef = fm.fourier_coefficients(B, seed=rank_seed(rank))
-    f, _ = fm.fourier_batch(n, coef, dtype, with_exact=False)
+    if nl:
+        f, _ = fm.nonlinear_batch(n, fm.nonlinear_scales(B, seed=rank_seed(rank)), dtype)
+    else:
+        coef = fm.fourier_coefficients(B, seed=rank_seed(rank))
+        f, _ = fm.fourier_batch(n, coef, dtype, with_exact=False)
     sol = torch.empty_like(f)
     stream = torch.cuda.current_stream()
 

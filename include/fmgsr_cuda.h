@@ -108,6 +108,21 @@ int fmgsr_tau_correction_f32(const float* u, float* out, int64_t n_fine, int64_t
 /* coarse_rhs, stencils.py:119-125: out = restrict(f) + tau(u) */
 int fmgsr_coarse_rhs_f64(const double* f, const double* u, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
 int fmgsr_coarse_rhs_f32(const float* f, const float* u, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+/* nonlinear variants (-u'' + u^3 = f; oracle/fmgsr_oracle.c defines them):
+ * coarse RHS with tau of N(u) = L u + u^3, Newton coarse solve (n <= 64),
+ * Newton-GS additive smoother (any ns; scratch as fmgsr_smooth_uniform) */
+int fmgsr_coarse_rhs_nl_f64(const double* f, const double* u, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_coarse_rhs_nl_f32(const float* f, const float* u, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
+int fmgsr_direct_solve_nl_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, void* stream);
+int fmgsr_direct_solve_nl_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, void* stream);
+int fmgsr_smooth_uniform_nl_f64(const double* u_in, const double* f, double* u_out, int64_t n,
+                                int64_t B, int64_t ld, int64_t W, int64_t b, int64_t ns,
+                                double omega, const double* uc, double proj_diag,
+                                double* scratch, int64_t sld, void* stream);
+int fmgsr_smooth_uniform_nl_f32(const float* u_in, const float* f, float* u_out, int64_t n,
+                                int64_t B, int64_t ld, int64_t W, int64_t b, int64_t ns,
+                                double omega, const float* uc, double proj_diag, float* scratch,
+                                int64_t sld, void* stream);
 /* FAS correction update, cycles.py:120-121: out = u + P(uH - R u) */
 int fmgsr_fas_correct_f64(const double* u, const double* uH, double* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
 int fmgsr_fas_correct_f32(const float* u, const float* uH, float* out, int64_t n_fine, int64_t B, int64_t ld, void* stream);
@@ -145,6 +160,8 @@ typedef struct fmgsr_plan_desc {
   int32_t use_graph;  /* 1: capture the cycle in a CUDA graph per (in, out) pair */
   int32_t coarse;     /* on-chip coarse hierarchy (fused, ns = 1 only): -1 auto cutoff,
                          0 off, k > 0: cutoff level Lc = k - 1 (capped by the smem budget) */
+  int32_t nonlinear;  /* 1: -u'' + u^3 = f (nonlinear FAS: Newton-GS, N(u) in tau, Newton
+                         coarse solve); the reference is linear only */
 } fmgsr_plan_desc;
 
 typedef struct fmgsr_plan_info {

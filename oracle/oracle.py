@@ -38,6 +38,7 @@ class OrcCfg(C.Structure):
         ("P", _i64),
         ("b", _i64),
         ("omega", C.c_double),
+        ("nonlin", C.c_int),
     ]
 
 
@@ -74,6 +75,12 @@ def lib():
         _lib.orc_fmg_solve.argtypes = [C.POINTER(OrcCfg), _dp, _dp]
         _lib.orc_fmg_solve_batch.argtypes = [C.POINTER(OrcCfg), _dp, _dp, _i64, C.c_int]
         _lib.orc_level_geometry.argtypes = [_i64, C.c_int, _i64, _i64, _ip, _ip]
+        _lib.orc_gs_sweep_nl.argtypes = [_dp, _dp, _i64, C.c_double, _i64, _i64, C.c_int,
+                                         C.c_double]
+        _lib.orc_apply_nonlinear.argtypes = [_dp, _dp, _i64]
+        _lib.orc_coarse_rhs_nl.argtypes = [_dp, _dp, _dp, _i64, _dp]
+        _lib.orc_direct_solve_nl.argtypes = [_dp, _dp, _i64, _dp]
+        _lib.orc_smooth_patches_nl.argtypes = _lib.orc_smooth_patches.argtypes
     return _lib
 
 
@@ -178,8 +185,56 @@ def level_geometry(n, mode, P=1, b=0):
     return int(W[0]), int(bb[0])
 
 
-def make_cfg(m0, m, n_sr=0, ns=1, mode=GEOM_PATCHES, P=1, b=0, omega=1.0):
-    return OrcCfg(m0, m, n_sr, ns, mode, P, b, omega)
+def make_cfg(m0, m, n_sr=0, ns=1, mode=GEOM_PATCHES, P=1, b=0, omega=1.0, nonlin=False):
+    return OrcCfg(m0, m, n_sr, ns, mode, P, b, omega, int(nonlin))
+
+
+# ---- nonlinear FAS restatement (-u'' + u^3 = f; see fmgsr_oracle.c) -------------------------
+def gs_sweep_nl(u, f, inv_h2, start, stop, forward, omega=1.0):
+    out = _f64(u).copy()
+    f = _f64(f)
+    lib().orc_gs_sweep_nl(_d(out), _d(f), len(out), float(inv_h2), start, stop, int(forward),
+                          omega)
+    return out
+
+
+def apply_nonlinear(u):
+    u = _f64(u)
+    out = np.empty_like(u)
+    lib().orc_apply_nonlinear(_d(u), _d(out), len(u))
+    return out
+
+
+def coarse_rhs_nl(f, u):
+    u = _f64(u)
+    f = _f64(f)
+    out = np.empty(len(u) // 2)
+    work = np.empty(3 * len(u) + 8)
+    lib().orc_coarse_rhs_nl(_d(f), _d(u), _d(out), len(u), _d(work))
+    return out
+
+
+def direct_solve_nl(f):
+    f = _f64(f)
+    out = np.empty_like(f)
+    work = np.empty(5 * len(f) + 8)
+    lib().orc_direct_solve_nl(_d(f), _d(out), len(f), _d(work))
+    return out
+
+
+def smooth_patches_nl(u, f, inv_h2, olo, ohi, elo, ehi, ns, omega=1.0, uc=None, proj_diag=0.5):
+    u = _f64(u)
+    f = _f64(f)
+    n = len(u)
+    out = np.empty(n)
+    scratch = np.empty(n)
+    arr = [np.ascontiguousarray(a, dtype=np.int64) for a in (olo, ohi, elo, ehi)]
+    ucv = _f64(uc) if uc is not None else np.zeros(1)
+    lib().orc_smooth_patches_nl(
+        _d(u), _d(f), _d(out), n, float(inv_h2), *[_i(a) for a in arr], len(arr[0]),
+        ns, omega, int(uc is not None), _d(ucv), proj_diag, _d(scratch),
+    )
+    return out
 
 
 def fmg_solve(cfg: OrcCfg, forcing):

@@ -88,7 +88,7 @@ def smooth_patches(u_in, f, inv_h2, owned_lo, owned_hi, ext_lo, ext_hi, ns, omeg
     return F.out(out, U)
 
 
-def smooth_uniform(u_in, f, W, b, ns, omega, u_coarse=None, proj_diag=0.5):
+def smooth_uniform(u_in, f, W, b, ns, omega, u_coarse=None, proj_diag=0.5, nonlinear=False):
     """Additive patch smoother over the uniform partition (W owned, b buffer)."""
     dt = F.pick_dtype(u_in, f)
     U = F.to_field(u_in, dt)
@@ -102,11 +102,12 @@ def smooth_uniform(u_in, f, W, b, ns, omega, u_coarse=None, proj_diag=0.5):
         uc_ptr = C.ptr()
     scratch = None
     sld = 0
-    if ns >= 2 or W % 2:
+    if ns >= 2 or W % 2 or nonlinear:
         rows = int(N.lib().fmgsr_smooth_scratch_rows(U.n, W, b))
         sld = ((U.B + 31) // 32) * 32
         scratch = torch.empty((max(rows, 1), sld), dtype=dt, device=U.t.device)
-    N.call("fmgsr_smooth_uniform", dt, U.ptr(), Fd.ptr(), out.data_ptr(), U.n, U.B, U.ld, int(W),
+    N.call("fmgsr_smooth_uniform_nl" if nonlinear else "fmgsr_smooth_uniform", dt, U.ptr(),
+           Fd.ptr(), out.data_ptr(), U.n, U.B, U.ld, int(W),
            int(b), int(ns), float(omega), uc_ptr, float(proj_diag),
            scratch.data_ptr() if scratch is not None else 0, sld, N.stream_ptr())
     return F.out(out, U)

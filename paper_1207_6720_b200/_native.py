@@ -32,6 +32,7 @@ class PlanDesc(C.Structure):
         ("geom_mode", _i32), ("dtype", _i32),
         ("P", _i64), ("b", _i64), ("B", _i64), ("ld", _i64),
         ("omega", _d), ("fused", _i32), ("use_graph", _i32), ("coarse", _i32),
+        ("nonlinear", _i32),
     ]
 
 
@@ -52,6 +53,10 @@ _SIGS = {
                                        _i64, _i64, _d, C.c_int, _vp, _d, _vp, _vp, _i64, _vp]),
     "fmgsr_smooth_uniform": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _d,
                                        _vp, _d, _vp, _i64, _vp]),
+    "fmgsr_smooth_uniform_nl": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _d,
+                                          _vp, _d, _vp, _i64, _vp]),
+    "fmgsr_coarse_rhs_nl": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_direct_solve_nl": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_apply_operator": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_restrict": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_prolong_correction": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
@@ -76,7 +81,8 @@ _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmg
           "fmgsr_apply_operator", "fmgsr_restrict", "fmgsr_prolong_correction",
           "fmgsr_prolong_fmg", "fmgsr_tau_correction", "fmgsr_coarse_rhs", "fmgsr_fas_correct",
           "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_fourier_rhs",
-          "fmgsr_nonlinear_rhs"}
+          "fmgsr_nonlinear_rhs", "fmgsr_smooth_uniform_nl", "fmgsr_coarse_rhs_nl",
+          "fmgsr_direct_solve_nl"}
 
 _lib = None
 _lock = threading.Lock()

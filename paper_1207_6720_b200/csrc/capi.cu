@@ -117,7 +117,7 @@ struct Plan : PlanBase {
       L.W = g.W;
       L.b = g.b;
       require(L.n % L.W == 0, "plan: owned width does not divide the level");
-      if (l > m0 && d.ns >= 2) {
+      if (l > m0 && (d.ns >= 2 || d.nonlinear)) {
         i64 rows = scratch_rows_uniform(L.n, L.W, L.b);
         if (rows > scratch_rows) scratch_rows = rows;
       }
@@ -151,7 +151,7 @@ struct Plan : PlanBase {
     check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
     // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
     // three fields per level (two u, f) for CW columns fit in ~200 KB.
-    use_coarse = d.fused && d.ns == 1 && d.coarse != 0;
+    use_coarse = d.fused && d.ns == 1 && d.coarse != 0 && !d.nonlinear;
     const char* tr = getenv("FMGSR_COARSE_TRACE");
     coarse_trace = (tr && tr[0] == '1') ? 1 : 0;
     if (use_coarse) {
@@ -253,11 +253,15 @@ struct Plan : PlanBase {
     ev.push_back(b);
   }
 
-  bool fused_restrict_ok(const Level& L) const { return d.fused && d.ns == 1 && L.W >= 4; }
+  bool fused_restrict_ok(const Level& L) const {
+    return d.fused && d.ns == 1 && L.W >= 4 && !d.nonlinear;
+  }
+  // fused prologue + ns = 1 chain (linear smoother only)
+  bool fused_chain_ok() const { return d.fused && d.ns == 1 && !d.nonlinear; }
 
   void smooth_into(int l, const T* u_in, const T* f, const T* uc, T* out, cudaStream_t s) {
     const Level& L = lv[l];
-    if (d.ns == 1) {
+    if (d.ns == 1 && !d.nonlinear) {
       VisitDesc<T> v;
       v.src = SRC_LOAD;
       v.cr = uc != nullptr;
@@ -288,6 +292,7 @@ struct Plan : PlanBase {
       c.out = out;
       c.scratch = scratch;
       c.sld = sld;
+      c.nonlinear = d.nonlinear != 0;
       launch_smooth_scratch(c, s);
     }
     n_launch++;
@@ -321,7 +326,7 @@ struct Plan : PlanBase {
       launch_visit(v, s);
       n_launch++;
       if (v.write_u) L.cur ^= 1;
-    } else if (d.fused && d.ns == 1) {
+    } else if (fused_chain_ok()) {
       VisitDesc<T> v;  // fused prolongation + smooth, separate restriction
       v.src = SRC_FMG;
       v.n = L.n;
@@ -336,14 +341,14 @@ struct Plan : PlanBase {
       launch_visit(v, s);
       n_launch++;
       L.cur ^= 1;
-      launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s);
+      launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s, d.nonlinear != 0);
       n_launch++;
     } else {
       launch_prolong_fmg(uH_in, tmp, H.n, d.ld, (int)d.B, s);
       n_launch++;
       smooth_into(t, tmp, ft, nullptr, L.u[L.cur ^ 1], s);
       L.cur ^= 1;
-      launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s);
+      launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s, d.nonlinear != 0);
       n_launch++;
     }
     H.cur ^= 1;
@@ -380,7 +385,8 @@ struct Plan : PlanBase {
     } else {
       smooth_into(l, L.u[L.cur], L.f, nullptr, L.u[L.cur ^ 1], s);
       L.cur ^= 1;
-      launch_restrict_tau(L.u[L.cur], L.f, H.u[H.cur ^ 1], H.f, L.n, d.ld, (int)d.B, 2, s);
+      launch_restrict_tau(L.u[L.cur], L.f, H.u[H.cur ^ 1], H.f, L.n, d.ld, (int)d.B, 2, s,
+                          d.nonlinear != 0);
       n_launch++;
       H.cur ^= 1;
     }
@@ -395,7 +401,7 @@ struct Plan : PlanBase {
     T* out = dst ? dst : L.u[L.cur ^ 1];
     const T* uH = H.u[H.cur];
     const bool sr = is_sr(l);
-    if (d.fused && d.ns == 1) {
+    if (fused_chain_ok()) {
       VisitDesc<T> v;
       v.src = sr ? SRC_FMG : SRC_CORR;
       v.cr = sr;
@@ -424,7 +430,8 @@ struct Plan : PlanBase {
   void visit_direct(cudaStream_t s) {
     Level& L = lv[d.m0];
     mark_begin(s, d.m0, VK_DIRECT);
-    launch_direct_solve(L.f, L.u[L.cur ^ 1], L.n, d.ld, (int)d.B, s);
+    if (d.nonlinear) launch_direct_solve_nl(L.f, L.u[L.cur ^ 1], L.n, d.ld, (int)d.B, s);
+    else launch_direct_solve(L.f, L.u[L.cur ^ 1], L.n, d.ld, (int)d.B, s);
     n_launch++;
     L.cur ^= 1;
     mark_end(s);
@@ -627,6 +634,7 @@ static void validate_desc(const fmgsr_plan_desc& d) {
   require(d.B >= 1 && d.ld >= d.B, "need 1 <= B <= ld");
   require(d.dtype == 0 || d.dtype == 1, "dtype must be 0 (f64) or 1 (f32)");
   require(((i64)1 << d.m0) <= 2048, "coarsest level above 2048 cells");
+  require(!d.nonlinear || ((i64)1 << d.m0) <= 64, "nonlinear: coarsest level above 64 cells");
 }
 
 }  // namespace fmgsr
@@ -772,6 +780,35 @@ int64_t fmgsr_smooth_scratch_rows(int64_t n, int64_t W, int64_t b) {
   }
 FMGSR_BOTH(fmgsr_smooth_uniform, SU_BODY)
 
+// nonlinear smoother (Newton-GS, any ns), staged windows
+#define SUNL_BODY(T)                                                                        \
+  (const T* u_in, const T* f, T* u_out, int64_t n, int64_t B, int64_t ld, int64_t W,          \
+   int64_t b, int64_t ns, double omega, const T* uc, double proj_diag, T* scratch,            \
+   int64_t sld, void* stream) {                                                              \
+    return guarded([&] {                                                                    \
+      check_field(n, B, ld, "smooth_uniform_nl");                                           \
+      require(u_in != u_out, "smooth_uniform_nl: u_out must not alias u_in");               \
+      ScratchDesc<T> c;                                                                     \
+      c.n = n;                                                                              \
+      c.ld = ld;                                                                            \
+      c.B = (int)B;                                                                         \
+      c.W = W;                                                                              \
+      c.b = b;                                                                              \
+      c.ns = ns;                                                                            \
+      c.omega = omega;                                                                      \
+      c.proj_diag = proj_diag;                                                              \
+      c.u_in = u_in;                                                                        \
+      c.f = f;                                                                              \
+      c.uc = uc;                                                                            \
+      c.out = u_out;                                                                        \
+      c.scratch = scratch;                                                                  \
+      c.sld = sld;                                                                          \
+      c.nonlinear = true;                                                                   \
+      launch_smooth_scratch(c, S(stream));                                                  \
+    });                                                                                     \
+  }
+FMGSR_BOTH(fmgsr_smooth_uniform_nl, SUNL_BODY)
+
 // ---- level operators -----------------------------------------------------------
 #define OP1(NAME, LAUNCH)                                                                   \
   int NAME##_f64(const double* a, double* out, int64_t n, int64_t B, int64_t ld, void* s) { \
@@ -796,6 +833,18 @@ int fmgsr_coarse_rhs_f64(const double* f, const double* u, double* out, int64_t 
 }
 int fmgsr_coarse_rhs_f32(const float* f, const float* u, float* out, int64_t n, int64_t B, int64_t ld, void* s) {
   return guarded([&] { check_field(n, B, ld, "coarse_rhs"); launch_restrict_tau<float>(u, f, nullptr, out, n, ld, (int)B, 1, S(s)); });
+}
+int fmgsr_coarse_rhs_nl_f64(const double* f, const double* u, double* out, int64_t n, int64_t B, int64_t ld, void* s) {
+  return guarded([&] { check_field(n, B, ld, "coarse_rhs_nl"); launch_restrict_tau<double>(u, f, nullptr, out, n, ld, (int)B, 1, S(s), true); });
+}
+int fmgsr_coarse_rhs_nl_f32(const float* f, const float* u, float* out, int64_t n, int64_t B, int64_t ld, void* s) {
+  return guarded([&] { check_field(n, B, ld, "coarse_rhs_nl"); launch_restrict_tau<float>(u, f, nullptr, out, n, ld, (int)B, 1, S(s), true); });
+}
+int fmgsr_direct_solve_nl_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, void* s) {
+  return guarded([&] { check_field(n, B, ld, "direct_solve_nl"); launch_direct_solve_nl<double>(f, u, n, ld, (int)B, S(s)); });
+}
+int fmgsr_direct_solve_nl_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, void* s) {
+  return guarded([&] { check_field(n, B, ld, "direct_solve_nl"); launch_direct_solve_nl<float>(f, u, n, ld, (int)B, S(s)); });
 }
 int fmgsr_fas_correct_f64(const double* u, const double* uH, double* out, int64_t n, int64_t B, int64_t ld, void* s) {
   return guarded([&] { check_field(n, B, ld, "fas_correct"); launch_fas_correct<double>(u, uH, out, n, ld, (int)B, S(s)); });

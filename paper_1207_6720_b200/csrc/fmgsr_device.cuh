@@ -75,6 +75,28 @@ __device__ __forceinline__ T gs_cell(const GsCoef<T>& c, i64 i, i64 n, T uL, T u
   return gs_int(c, uL, u, uR, f);
 }
 
+// Nonlinear (-u'' + u^3 = f) Gauss-Seidel: one pointwise Newton step,
+// r = f - (inv_h2*s + (u*u)*u), J = diag + 3(u*u), u += (omega*r)/J
+// (oracle/fmgsr_oracle.c orc_gs_sweep_nl; the reference is linear only).
+template <typename T>
+__device__ __forceinline__ T gs_cell_nl(const GsCoef<T>& c, i64 i, i64 n, T uL, T u, T uR, T f) {
+  T s, diag;
+  if (i == 0) {
+    s = xsub(xmul(T(3), u), uR);
+    diag = c.diag_b;
+  } else if (i == n - 1) {
+    s = xsub(xmul(T(3), u), uL);
+    diag = c.diag_b;
+  } else {
+    s = xsub(xsub(xmul(T(2), u), uL), uR);
+    diag = xmul(T(2), c.inv_h2);
+  }
+  T uu = xmul(u, u);
+  T r = xsub(f, xadd(xmul(c.inv_h2, s), xmul(uu, u)));
+  T J = xadd(diag, xmul(T(3), uu));
+  return xadd(u, xdiv(xmul(c.omega, r), J));
+}
+
 // Kaczmarz projection of one pair onto its coarse value, reference
 // _kernels_numba.py:53-56: r = uc - 0.5(a+b); t = r/proj_diag; a,b += 0.5 t.
 // When proj_diag is a power of two (the reference's 0.5) the division is an

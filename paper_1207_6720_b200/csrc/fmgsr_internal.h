@@ -142,6 +142,7 @@ struct ScratchDesc {
   T* out = nullptr;
   T* scratch = nullptr;
   i64 sld = 0;  // scratch row stride (>= round_up(B, 32))
+  bool nonlinear = false;  // Newton-GS for -u'' + u^3 = f
 };
 
 template <typename T>
@@ -153,8 +154,11 @@ template <typename T> void launch_apply_operator(const T* u, T* out, i64 n, i64 
 template <typename T> void launch_restrict(const T* u, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_prolong_correction(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_prolong_fmg(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t s);
-// mode 0: tau only; 1: coarse_rhs; 2: restrict + coarse_rhs (uH_out, fH_out)
-template <typename T> void launch_restrict_tau(const T* u, const T* f, T* uH_out, T* fH_out, i64 nf, i64 ld, int B, int mode, cudaStream_t s);
+// mode 0: tau only; 1: coarse_rhs; 2: restrict + coarse_rhs (uH_out, fH_out);
+// nl: tau of the nonlinear operator N(u) = L u + u^3
+template <typename T> void launch_restrict_tau(const T* u, const T* f, T* uH_out, T* fH_out, i64 nf, i64 ld, int B, int mode, cudaStream_t s, bool nl = false);
+// Newton solve of L u + u^3 = f on the coarsest level (n <= 64)
+template <typename T> void launch_direct_solve_nl(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s, T* workspace = nullptr);
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);

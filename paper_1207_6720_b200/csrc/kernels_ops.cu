@@ -128,7 +128,7 @@ __global__ void k_prolong_fmg(const T* __restrict__ c, T* __restrict__ out, i64 
 // stencils.py:108-125.  mode 0: tau; 1: coarse_rhs; 2: restrict + coarse_rhs.
 template <typename T>
 __global__ void k_restrict_tau(const T* __restrict__ u, const T* __restrict__ f, T* __restrict__ uH,
-                               T* __restrict__ fH, i64 nf, i64 ld, int B, int mode) {
+                               T* __restrict__ fH, i64 nf, i64 ld, int B, int mode, bool nl) {
   int r = blockIdx.x * TX + threadIdx.x;
   if (r >= B) return;
   const i64 nc = nf / 2;
@@ -140,7 +140,14 @@ __global__ void k_restrict_tau(const T* __restrict__ u, const T* __restrict__ f,
     if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru_at(ur, 1, ld)), iH);
     else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rj), ru_at(ur, nc - 2, ld)), iH);
     else LH = xmul(xsub(xsub(xmul(T(2), Rj), ru_at(ur, j - 1, ld)), ru_at(ur, j + 1, ld)), iH);
-    T RL = xmul(T(0.5), xadd(lu_at(ur, 2 * j, nf, ld, ih), lu_at(ur, 2 * j + 1, nf, ld, ih)));
+    T L0 = lu_at(ur, 2 * j, nf, ld, ih), L1 = lu_at(ur, 2 * j + 1, nf, ld, ih);
+    if (nl) {  // N(u) = L u + u^3 on both levels (orc_coarse_rhs_nl)
+      T a = ur[(2 * j) * ld], b = ur[(2 * j + 1) * ld];
+      L0 = xadd(L0, xmul(xmul(a, a), a));
+      L1 = xadd(L1, xmul(xmul(b, b), b));
+      LH = xadd(LH, xmul(xmul(Rj, Rj), Rj));
+    }
+    T RL = xmul(T(0.5), xadd(L0, L1));
     T tau = xsub(LH, RL);
     if (mode == 0) {
       fH[j * ld + r] = tau;
@@ -348,10 +355,66 @@ void launch_prolong_fmg(const T* c, T* out, i64 nc, i64 ld, int B, cudaStream_t 
 }
 template <typename T>
 void launch_restrict_tau(const T* u, const T* f, T* uH, T* fH, i64 nf, i64 ld, int B, int mode,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool nl) {
   require(nf >= 4 && is_pow2(nf), "tau: fine size must be a power of two >= 4");
-  k_restrict_tau<T><<<grid_for(nf / 2, B), dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode);
+  k_restrict_tau<T><<<grid_for(nf / 2, B), dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode, nl);
   check_launch("restrict_tau");
+}
+
+// Newton solve of N(u) = L u + u^3 = f (orc_direct_solve_nl): linear solve as
+// the first iterate, then NEWTON_STEPS steps, each a tridiagonal L + diag(3u^2)
+// solve in the dpttrf / dptts2 order.  One thread per RHS; u lives in the
+// output column, the factor and residual in per-thread local arrays.
+constexpr int NEWTON_STEPS = 10;
+constexpr int NEWTON_NMAX = 64;
+
+template <typename T>
+__global__ void k_direct_solve_nl(const T* __restrict__ f, T* __restrict__ u, i64 n, i64 ld, int B) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  T d[NEWTON_NMAX], e[NEWTON_NMAX], rr[NEWTON_NMAX];
+  const T ih = inv_h2_of<T>(n);
+  const T* fr = f + r;
+  T* ur = u + r;
+  // linear first iterate (k_direct_solve)
+  pt_factor(d, e, n);
+  T prev = fr[0];
+  ur[0] = prev;
+  for (i64 i = 1; i < n; i++) {
+    prev = xsub(fr[i * ld], xmul(prev, e[i - 1]));
+    ur[i * ld] = prev;
+  }
+  T nx = xdiv(prev, d[n - 1]);
+  ur[(n - 1) * ld] = nx;
+  for (i64 i = n - 2; i >= 0; i--) {
+    nx = xsub(xdiv(ur[i * ld], d[i]), xmul(nx, e[i]));
+    ur[i * ld] = nx;
+  }
+  for (int it = 0; it < NEWTON_STEPS; it++) {
+    for (i64 i = 0; i < n; i++) {
+      T ui = ur[i * ld];
+      T Ni = xadd(lu_at(ur, i, n, ld, ih), xmul(xmul(ui, ui), ui));
+      rr[i] = xsub(fr[i * ld], Ni);
+      d[i] = xadd(xmul(T((i == 0 || i == n - 1) ? 3 : 2), ih), xmul(T(3), xmul(ui, ui)));
+      e[i] = -ih;
+    }
+    for (i64 i = 0; i < n - 1; i++) {
+      T ei = e[i];
+      e[i] = xdiv(ei, d[i]);
+      d[i + 1] = xsub(d[i + 1], xmul(e[i], ei));
+    }
+    for (i64 i = 1; i < n; i++) rr[i] = xsub(rr[i], xmul(rr[i - 1], e[i - 1]));
+    rr[n - 1] = xdiv(rr[n - 1], d[n - 1]);
+    for (i64 i = n - 2; i >= 0; i--) rr[i] = xsub(xdiv(rr[i], d[i]), xmul(rr[i + 1], e[i]));
+    for (i64 i = 0; i < n; i++) ur[i * ld] = xadd(ur[i * ld], rr[i]);
+  }
+}
+
+template <typename T>
+void launch_direct_solve_nl(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s) {
+  require(n >= 2 && is_pow2(n) && n <= NEWTON_NMAX, "nonlinear direct solve: n must be a power of two in [2, 64]");
+  k_direct_solve_nl<T><<<(B + 127) / 128, 128, 0, s>>>(f, u, n, ld, B);
+  check_launch("direct_solve_nl");
 }
 template <typename T>
 void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s) {
@@ -421,7 +484,8 @@ void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* ue
   template void launch_prolong_correction<T>(const T*, T*, i64, i64, int, cudaStream_t);      \
   template void launch_prolong_fmg<T>(const T*, T*, i64, i64, int, cudaStream_t);             \
   template void launch_restrict_tau<T>(const T*, const T*, T*, T*, i64, i64, int, int,        \
-                                       cudaStream_t);                                          \
+                                       cudaStream_t, bool);                                    \
+  template void launch_direct_solve_nl<T>(const T*, T*, i64, i64, int, cudaStream_t);          \
   template void launch_fas_correct<T>(const T*, const T*, T*, i64, i64, int, cudaStream_t);   \
   template void launch_direct_solve<T>(const T*, T*, i64, i64, int, cudaStream_t, T*);            \
   template void launch_gs_sweep<T>(T*, const T*, i64, i64, int, double, i64, i64, bool,       \

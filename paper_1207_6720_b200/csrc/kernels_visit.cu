@@ -287,7 +287,7 @@ struct ScratchArgs {
   T *out, *scratch;
 };
 
-template <typename T, bool CR>
+template <typename T, bool CR, bool NL>
 __global__ void __launch_bounds__(128) smooth_scratch_kernel(const ScratchArgs<T> a) {
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -336,7 +336,8 @@ __global__ void __launch_bounds__(128) smooth_scratch_kernel(const ScratchArgs<T
       T cur = S(ws);
       for (i64 i = ws; i < we; i++) {
         T nxt = (i + 1 < hi) ? S(i + 1) : T(0);
-        T v = gs_cell(a.gc, i, n, uL, cur, nxt, ldg(f + i * ld));
+        T v = NL ? gs_cell_nl(a.gc, i, n, uL, cur, nxt, ldg(f + i * ld))
+                 : gs_cell(a.gc, i, n, uL, cur, nxt, ldg(f + i * ld));
         S(i) = v;
         uL = v;
         cur = nxt;
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(128) smooth_scratch_kernel(const ScratchArgs<T
       T cur = S(we - 1);
       for (i64 i = we - 1; i >= ws; i--) {
         T prv = (i - 1 >= lo) ? S(i - 1) : T(0);
-        T v = gs_cell(a.gc, i, n, prv, cur, uR, ldg(f + i * ld));
+        T v = NL ? gs_cell_nl(a.gc, i, n, prv, cur, uR, ldg(f + i * ld))
+                 : gs_cell(a.gc, i, n, prv, cur, uR, ldg(f + i * ld));
         S(i) = v;
         uR = v;
         cur = prv;
@@ -399,8 +401,13 @@ void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s) {
   }
   if (a.P == 0) return;
   i64 blocks = (a.P * a.nrg + 3) / 4;
-  if (d.uc) smooth_scratch_kernel<T, true><<<(unsigned)blocks, 128, 0, s>>>(a);
-  else smooth_scratch_kernel<T, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+  if (d.nonlinear) {
+    if (d.uc) smooth_scratch_kernel<T, true, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+    else smooth_scratch_kernel<T, false, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+  } else {
+    if (d.uc) smooth_scratch_kernel<T, true, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+    else smooth_scratch_kernel<T, false, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+  }
   check_launch("smooth_scratch_kernel");
 }
 

@@ -82,7 +82,7 @@ def down_leg(k: int, state: CycleState, cfg: SolverConfig) -> CycleState:
     for l in range(k, m0, -1):
         u_fine = state.u[l]
         state.u[l - 1] = restrict(u_fine)
-        state.f_work[l - 1] = coarse_rhs(state.f_work[l], u_fine)
+        state.f_work[l - 1] = coarse_rhs(state.f_work[l], u_fine, cfg.smoother.nonlinear)
         state.u[l - 1] = smooth_level(state.u[l - 1], state.f_work[l - 1], cfg.smoother, m0)
     return state
 
@@ -121,7 +121,7 @@ def _operator_path(cfg, forcing, collect_diagnostics, debug_sr):
     for k in range(m - 1, m0 - 1, -1):
         f_orig[k] = restrict(f_orig[k + 1])
     state = CycleState(u={}, f_work={}, f_orig=f_orig)
-    state.u[m0] = direct_solve(f_orig[m0])
+    state.u[m0] = direct_solve(f_orig[m0], nonlinear=cfg.smoother.nonlinear)
     state.f_work[m0] = f_orig[m0]
     diag = Diagnostics()
     for k in range(m0, m):

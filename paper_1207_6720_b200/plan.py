@@ -35,6 +35,7 @@ class PlanKey:
     fused: bool = True
     use_graph: bool = True
     coarse: int = -1  # on-chip coarse hierarchy: -1 auto, 0 off, k > 0 cutoff level k - 1
+    nonlinear: bool = False  # -u'' + u^3 = f
 
 
 def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
@@ -52,7 +53,7 @@ def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
         mode, P = GEOM_HALO, 1
         b = sm.buffer if sm.buffer is not None else sm.halo_mode.halo
     return PlanKey(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns, mode, int(P), int(b),
-                   int(B), dtype, float(sm.omega), fused, use_graph, coarse)
+                   int(B), dtype, float(sm.omega), fused, use_graph, coarse, bool(sm.nonlinear))
 
 
 class FmgPlan:
@@ -68,6 +69,7 @@ class FmgPlan:
         d.fused = int(key.fused)
         d.use_graph = int(key.use_graph)
         d.coarse = int(key.coarse)
+        d.nonlinear = int(key.nonlinear)
         h = C.c_void_p()
         N.check(N.lib().fmgsr_plan_create(C.byref(d), C.byref(h)), "plan_create")
         self._h = h

@@ -32,6 +32,8 @@ class SmootherConfig:
     reference partition; omega: relaxation weight (1.0 in every study).
     n_patches / buffer: the P-patch geometry W_l = max(2, n_l/P) with a
     b-cell buffer; when n_patches is None the reference partition is used.
+    nonlinear: solve -u'' + u^3 = f (BASELINE config 3) instead of -u'' = f;
+    the reference is linear only, the restatement is oracle/fmgsr_oracle.c.
     """
 
     ns: int = 1
@@ -39,6 +41,7 @@ class SmootherConfig:
     omega: float = 1.0
     n_patches: int | None = None
     buffer: int | None = None
+    nonlinear: bool = False  # -u'' + u^3 = f: Newton-GS smoother, Newton coarse solve
 
     def __post_init__(self) -> None:
         if self.ns < 1:
@@ -115,7 +118,7 @@ def smooth_level(u, f, cfg: SmootherConfig, m0: int, cr: CrContext | None = None
     if k < m0:
         raise ValueError(f"level {k} below the coarsest level {m0}")
     if k == m0:
-        return direct_solve(f)
+        return direct_solve(f, nonlinear=cfg.nonlinear)
     n = F.length(u)
     if cr is not None:
         if 2 * F.length(cr.u_coarse) != n:
@@ -126,7 +129,10 @@ def smooth_level(u, f, cfg: SmootherConfig, m0: int, cr: CrContext | None = None
         g = cfg.geometry(n)
         return lane.smooth_uniform(u, f, g.W, g.b, cfg.ns, cfg.omega,
                                    cr.u_coarse if cr is not None else None,
-                                   cr.proj_diag if cr is not None else 1.0)
+                                   cr.proj_diag if cr is not None else 1.0,
+                                   nonlinear=cfg.nonlinear)
+    if cfg.nonlinear:
+        raise ValueError("explicit patch lists are not supported for the nonlinear smoother")
     owned_lo, owned_hi, ext_lo, ext_hi = patch_arrays(list(patches))
     order = np.argsort(owned_lo)
     covered = np.all(owned_lo[order][1:] == owned_hi[order][:-1])
@@ -138,13 +144,19 @@ def smooth_level(u, f, cfg: SmootherConfig, m0: int, cr: CrContext | None = None
                                cr.proj_diag if cr is not None else 1.0)
 
 
-def direct_solve(f):
-    """Exact solve of the level operator (smoothers.py:210-225; LAPACK ?ptsv order)."""
+def direct_solve(f, nonlinear: bool = False):
+    """Exact solve of the level operator (smoothers.py:210-225; LAPACK ?ptsv order).
+    ``nonlinear``: Newton solve of L u + u^3 = f (n <= 64)."""
     stencils.level_of(f)
     dt = F.pick_dtype(f)
     Fd = F.to_field(f, dt)
     out = torch.empty_like(Fd.t)
-    if Fd.n <= 2048:
+    if nonlinear:
+        if Fd.n > 64:
+            raise ValueError(f"nonlinear direct solve supports at most 64 cells, got {Fd.n}")
+        N.call("fmgsr_direct_solve_nl", dt, Fd.ptr(), out.data_ptr(), Fd.n, Fd.B, Fd.ld,
+               N.stream_ptr())
+    elif Fd.n <= 2048:
         N.call("fmgsr_direct_solve", dt, Fd.ptr(), out.data_ptr(), Fd.n, Fd.B, Fd.ld,
                N.stream_ptr())
     else:

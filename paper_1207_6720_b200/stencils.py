@@ -65,8 +65,8 @@ def tau_correction(u_fine):
     return _unary("fmgsr_tau_correction", u_fine, lambda n: n // 2)
 
 
-def coarse_rhs(f_fine, u_fine):
-    """R f + tau(u) (stencils.py:119-125)."""
+def coarse_rhs(f_fine, u_fine, nonlinear: bool = False):
+    """R f + tau(u) (stencils.py:119-125); ``nonlinear``: tau of N(u) = L u + u^3."""
     if F.length(f_fine) != F.length(u_fine):
         raise ValueError(
             f"forcing and solution sizes differ: {F.length(f_fine)} vs {F.length(u_fine)}")
@@ -77,8 +77,8 @@ def coarse_rhs(f_fine, u_fine):
     U = F.to_field(u_fine, dt)
     F.same_batch(Fd, U)
     out = F.empty_like_rows(U, U.n // 2)
-    N.call("fmgsr_coarse_rhs", dt, Fd.ptr(), U.ptr(), out.data_ptr(), U.n, U.B, U.ld,
-           N.stream_ptr())
+    N.call("fmgsr_coarse_rhs_nl" if nonlinear else "fmgsr_coarse_rhs", dt, Fd.ptr(), U.ptr(),
+           out.data_ptr(), U.n, U.B, U.ld, N.stream_ptr())
     return F.out(out, U)
 
 

@@ -141,3 +141,59 @@ def test_geometry_rule_reproduces_reference_partition(oracle):
         assert oracle.level_geometry(n, oracle.GEOM_HALO, 1, 2) == (2, 2)
         assert oracle.level_geometry(n, oracle.GEOM_GLOBAL, 1, 0) == (n, 0)
     assert oracle.level_geometry(2 ** 16, oracle.GEOM_PATCHES, 64, 4) == (1024, 4)
+
+
+# ---- nonlinear FAS restatement (config 3; the reference is linear only) -------------------
+def _newton_fine(oracle, f):
+    """Discrete solution of L u + u^3 = f by Newton with a banded LU (independent)."""
+    n = len(f)
+    inv = float(n * n)
+    u = np.zeros(n)
+    for _ in range(30):
+        r = f - (oracle.apply_operator(u) + u ** 3)
+        ab = np.zeros((3, n))
+        ab[0, 1:] = -inv
+        ab[1, :] = 2 * inv + 3 * u ** 2
+        ab[1, 0] = 3 * inv + 3 * u[0] ** 2
+        ab[1, -1] = 3 * inv + 3 * u[-1] ** 2
+        ab[2, :-1] = -inv
+        u = u + solve_banded((1, 1), ab, r)
+    return u
+
+
+@pytest.mark.parametrize("ns", [1, 2])
+def test_nonlinear_one_cycle_truncation_accuracy(oracle, ns):
+    """Manufactured u = s x(1-x)e^x: one FMG cycle lands within 2x of the
+    discrete solution's discretisation error, at second order."""
+    errs = []
+    for m in (8, 10, 12):
+        n = 2 ** m
+        x = (np.arange(n) + 0.5) / n
+        s = 1.7
+        u = s * x * (1 - x) * np.exp(x)
+        f = s * x * (x + 3) * np.exp(x) + u ** 3
+        cfg = oracle.make_cfg(3, m, 1, ns, oracle.GEOM_PATCHES, min(256, n // 4), 4, nonlin=True)
+        sol = oracle.fmg_solve(cfg, f)
+        e = np.linalg.norm(sol - u) / np.linalg.norm(u)
+        ed = np.linalg.norm(_newton_fine(oracle, f) - u) / np.linalg.norm(u)
+        assert e <= 2.0 * ed
+        errs.append(e)
+    assert errs[0] / errs[1] > 10 and errs[1] / errs[2] > 10  # ~16 per two levels
+
+
+def test_nonlinear_coarse_newton_solves(oracle):
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal(8) * 50
+    u = oracle.direct_solve_nl(f)
+    assert np.max(np.abs(oracle.apply_nonlinear(u) - f)) < 1e-12 * np.max(np.abs(f))
+
+
+def test_nonlinear_reduces_to_linear_for_tiny_fields(oracle):
+    """With u ~ 1e-8 the cubic term is below rounding: the nonlinear sweep
+    equals the linear one to ~1e-15 relative."""
+    rng = np.random.default_rng(9)
+    u = rng.standard_normal(32) * 1e-8
+    f = rng.standard_normal(32) * 1e-8
+    a = oracle.gs_sweep(u, f, 4.0 ** 5, 0, 32, True)
+    b = oracle.gs_sweep_nl(u, f, 4.0 ** 5, 0, 32, True)
+    assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(a))
