@@ -331,7 +331,7 @@ def run_gpu(args, w):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": w["dtype"], "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
+            "dtype": w["dtype"], "data": ("synthetic (seeded manufactured nonlinear RHS, s ~ U[0.5, 2])" if nl else "synthetic (seeded Fourier RHS, SURVEY 8(d))"),
             "config": workload_config(args.workload, w, world),
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
