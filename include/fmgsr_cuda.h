@@ -194,6 +194,30 @@ int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void
                            float* visit_ms, int32_t* visit_level, int32_t* visit_kind,
                            int64_t cap, int64_t* n_visits);
 
+/* ---- Patch-slab sharding -----------------------------------
+ * One problem split into S contiguous slabs of patches on every level above a
+ * replication cutoff Lr (chosen by the plan: every level above it splits into
+ * whole patches of owned width >= 4 with room for the halo); levels <= Lr are
+ * solved redundantly by every shard.  Each sharded visit is followed by one
+ * exchange of halo rows and slab-edge tau records with the two neighbours;
+ * the visit into Lr is followed by an all-gather of the restricted level.
+ * Fused ns = 1 linear path only (desc->fused = 1, ns = 1, nonlinear = 0). */
+/* One shard per GPU over NCCL (libnccl.so.2 is loaded on first use).  The
+ * 128-byte id comes from fmgsr_nccl_unique_id on one rank, broadcast to all.
+ * The returned plan is driven by fmgsr_plan_solve with the rank's SLAB of the
+ * forcing and of the solution: DEVICE [2^m / shards][ld]. */
+int fmgsr_nccl_unique_id(void* id /* 128 bytes */);
+int fmgsr_shard_plan_create(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                            const void* nccl_id, void** plan);
+/* Virtual shards: all S shards of one problem on the current device, run in
+ * lockstep on one stream (transfers are device copies).  forcing / solution
+ * are the full DEVICE [2^m][ld] arrays; the result is bit-identical to the
+ * unsharded plan. */
+int fmgsr_shard_group_create(const fmgsr_plan_desc* desc, int32_t shards, void** group);
+int fmgsr_shard_group_solve(void* group, const void* forcing, void* solution, void* stream);
+int fmgsr_shard_group_cutoff(void* group, int32_t* cutoff, int64_t* halo_rows);
+int fmgsr_shard_group_destroy(void* group);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,12 @@ _SIGS = {
     "fmgsr_plan_solve_host": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "fmgsr_plan_solve_timed": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                                          C.POINTER(_i64)]),
+    "fmgsr_nccl_unique_id": (C.c_int, [_vp]),
+    "fmgsr_shard_plan_create": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, _vp, C.POINTER(_vp)]),
+    "fmgsr_shard_group_create": (C.c_int, [C.POINTER(PlanDesc), _i32, C.POINTER(_vp)]),
+    "fmgsr_shard_group_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "fmgsr_shard_group_cutoff": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i64)]),
+    "fmgsr_shard_group_destroy": (C.c_int, [_vp]),
 }
 _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmgsr_smooth_uniform",
           "fmgsr_apply_operator", "fmgsr_restrict", "fmgsr_prolong_correction",

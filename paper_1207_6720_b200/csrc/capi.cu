@@ -7,6 +7,8 @@
 // the visit qualifies (ns = 1, owned width >= 4 for visits that restrict),
 // and captures the whole cycle into a CUDA graph that is replayed per solve.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -51,6 +53,29 @@ static LevelGeo level_geometry(i64 n, int mode, i64 P, i64 b) {
   return {w < 2 ? 2 : w, b};
 }
 
+// ---------------------------------------------------------------------------
+// Patch-slab sharding transport.  A sharded plan owns one contiguous slab of
+// patches on every level above the replication cutoff Lr; after each visit
+// it exchanges halo rows and slab-edge tau records with its two neighbours
+// and, at Lr, all-gathers the restricted level so everything below runs
+// replicated.  Transfers are described, not performed, by the plan:
+// ShardGroup (virtual shards on one device) turns them into device copies,
+// NcclComm (one shard per GPU) into grouped ncclSend / ncclRecv / ncclAllGather.
+// ---------------------------------------------------------------------------
+struct Xfer {
+  int peer;
+  bool send;
+  void* ptr;
+  size_t bytes;
+  int tag;
+};
+struct Gather {
+  char* base;    // the full (replicated) array
+  size_t chunk;  // bytes owned by each shard, shard k at base + k * chunk
+};
+
+struct NcclApi;  // dlopen'ed libnccl (only when a multi-GPU sharded plan is built)
+
 struct PlanBase {
   fmgsr_plan_desc d{};
   virtual ~PlanBase() {}
@@ -92,6 +117,16 @@ struct Plan : PlanBase {
   bool use_coarse = false;
   int Lc = 0, CW = 1;
   int coarse_trace = 0;
+  // patch-slab sharding: levels > Lr are split into S slabs, this is slab srank;
+  // slab arrays carry H halo rows per side and are addressed through
+  // "virtual global" pointers (global row g at base + (g - c0 + H) * ld)
+  int S = 1, srank = 0, Lr = 1 << 30;
+  i64 H = 0;
+  T* fm = nullptr;  // sharded finest forcing (slab + halo)
+  std::vector<T*> ob, ib;  // per-level edge-record outbox / inbox (2 slots x 5 x Bp)
+  bool sharded(int l) const { return S > 1 && l > Lr; }
+  i64 c0(int l) const { return (lv[l].n / S) * srank; }
+  i64 c1(int l) const { return (lv[l].n / S) * (srank + 1); }
 
   bool is_sr(int l) const { return l > d.m - d.n_sr; }
 
@@ -103,8 +138,10 @@ struct Plan : PlanBase {
     return (T*)p;
   }
 
-  explicit Plan(const fmgsr_plan_desc& desc) {
+  explicit Plan(const fmgsr_plan_desc& desc, int shards = 1, int shard = 0) {
     d = desc;
+    S = shards;
+    srank = shard;
     const int m0 = d.m0, m = d.m;
     const i64 ld = d.ld, Bp = ((d.B + 31) / 32) * 32;
     const int nrg = (int)(Bp / 32);
@@ -124,31 +161,6 @@ struct Plan : PlanBase {
       if (l > m0) tmp_rows = L.n > tmp_rows ? L.n : tmp_rows;
       if (l > m0 && L.W >= 4) cnt_total += (L.n / L.W + 1) * nrg;
     }
-    for (int l = m0; l <= m; l++) {
-      Level& L = lv[l];
-      size_t fb = (size_t)L.n * ld * sizeof(T);
-      L.u[0] = alloc(fb);
-      L.u[1] = alloc(fb);
-      if (l < m) L.f = alloc(fb);
-      if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
-    }
-    tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
-    if (scratch_rows) {
-      sld = Bp;
-      scratch = alloc((size_t)scratch_rows * sld * sizeof(T));
-    }
-    cnt_bytes = (size_t)cnt_total * sizeof(int);
-    cnt_all = (int*)alloc(cnt_bytes);
-    check_cuda(cudaMemset(cnt_all, 0, cnt_bytes ? cnt_bytes : 16), "plan memset");
-    i64 off = 0;
-    for (int l = m0 + 1; l <= m; l++) {
-      Level& L = lv[l];
-      if (L.W >= 4) {
-        L.cnt = cnt_all + off;
-        off += (L.n / L.W + 1) * nrg;
-      }
-    }
-    check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
     // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
     // three fields per level (two u, f) for CW columns fit in ~200 KB.
     use_coarse = d.fused && d.ns == 1 && d.coarse != 0 && !d.nonlinear;
@@ -168,6 +180,91 @@ struct Plan : PlanBase {
         if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
       if (want > 0 && want - 1 >= m0 && want - 1 < Lc) Lc = want - 1;
     }
+    if (S > 1) {
+      plan_shards(Bp);
+      finish_shards();
+    }
+    ob.assign(m + 1, nullptr);
+    ib.assign(m + 1, nullptr);
+    for (int l = m0; l <= m; l++) {
+      Level& L = lv[l];
+      if (sharded(l)) {
+        // slab + halo; pointers stored shifted to virtual global rows
+        const i64 rows = L.n / S + 2 * H, shift = (H - c0(l)) * ld;
+        size_t fb = (size_t)rows * ld * sizeof(T);
+        L.u[0] = alloc(fb) + shift;
+        L.u[1] = alloc(fb) + shift;
+        if (l < m) L.f = alloc(fb) + shift;
+        else fm = alloc(fb) + shift;
+        ob[l] = alloc((size_t)10 * Bp * sizeof(T));
+        ib[l] = alloc((size_t)10 * Bp * sizeof(T));
+      } else {
+        size_t fb = (size_t)L.n * ld * sizeof(T);
+        L.u[0] = alloc(fb);
+        L.u[1] = alloc(fb);
+        if (l < m) L.f = alloc(fb);
+      }
+      if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
+    }
+    tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
+    if (scratch_rows) {
+      sld = Bp;
+      scratch = alloc((size_t)scratch_rows * sld * sizeof(T));
+    }
+    cnt_bytes = (size_t)cnt_total * sizeof(int);
+    cnt_all = (int*)alloc(cnt_bytes);
+    check_cuda(cudaMemset(cnt_all, 0, cnt_bytes ? cnt_bytes : 16), "plan memset");
+    i64 off = 0;
+    for (int l = m0 + 1; l <= m; l++) {
+      Level& L = lv[l];
+      if (L.W >= 4) {
+        L.cnt = cnt_all + off;
+        off += (L.n / L.W + 1) * nrg;
+      }
+    }
+    check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
+  }
+
+  // Replication cutoff: every level above Lr must split into S slabs of whole
+  // patches with owned width >= 4 (fused restriction epilogue) and room for
+  // the halo; Lr >= Lc (the on-chip levels are replicated anyway).
+  void plan_shards(i64 Bp) {
+    (void)Bp;
+    require(d.fused && d.ns == 1 && !d.nonlinear && d.coarse != 0,
+            "sharding needs the fused ns = 1 linear path");
+    require(S >= 2 && is_pow2(S) && srank >= 0 && srank < S, "bad shard count / index");
+    H = d.b + 8;
+    H += H & 1;
+    auto ok = [&](int l) {
+      const Level& L = lv[l];
+      const i64 slab = L.n / S;
+      return L.n % S == 0 && slab % L.W == 0 && L.W >= 4 && slab >= 2 * H && slab >= 64;
+    };
+    require(ok(d.m), "sharding: the finest level cannot be split into S patch slabs");
+    int l = d.m;
+    while (l - 1 > d.m0 && ok(l - 1)) l--;
+    Lr = l - 1;
+  }
+  void finish_shards() {  // after the coarse cutoff is known
+    if (S > 1 && Lr < Lc) {
+      // levels Lr+1..Lc would be both sharded and on chip: shard only above Lc
+      Lr = Lc;
+      require(Lr < d.m, "sharding: nothing left above the coarse cutoff");
+    }
+  }
+  void shard_desc(VisitDesc<T>& v, int l) const {
+    if (!sharded(l)) return;
+    const Level& L = lv[l];
+    v.p_begin = c0(l) / L.W;
+    v.p_count = (c1(l) - c0(l)) / L.W;
+    const i64 lo = c0(l) - H, hi = c1(l) + H;  // rows in memory
+    v.qlo = lo < 0 ? 0 : lo / 2;
+    v.qhi = (hi > L.n ? L.n : hi) / 2 - 1;
+    if (v.epi) {
+      v.E_out = ob[l];
+      v.left_remote = c0(l) > 0;
+      v.right_remote = c1(l) < L.n;
+    }
   }
 
   ~Plan() override {
@@ -177,6 +274,7 @@ struct Plan : PlanBase {
     if (cap) cudaStreamDestroy(cap);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
+    if (ncomm && nccl && nccl->commDestroy) nccl->commDestroy(ncomm);
     for (void* p : allocs) cudaFree(p);
   }
 
@@ -323,6 +421,7 @@ struct Plan : PlanBase {
       v.fH_out = H.f;
       v.E = L.E;
       v.cnt = L.cnt;
+      shard_desc(v, t);
       launch_visit(v, s);
       n_launch++;
       if (v.write_u) L.cur ^= 1;
@@ -378,6 +477,7 @@ struct Plan : PlanBase {
       v.fH_out = H.f;
       v.E = L.E;
       v.cnt = L.cnt;
+      shard_desc(v, l);
       launch_visit(v, s);
       n_launch++;
       if (v.write_u) L.cur ^= 1;
@@ -415,6 +515,7 @@ struct Plan : PlanBase {
       v.uH = uH;
       v.f = fl;
       v.u_out = out;
+      shard_desc(v, l);
       launch_visit(v, s);
       n_launch++;
     } else {
@@ -440,29 +541,16 @@ struct Plan : PlanBase {
   // One full FMG pass (cycles.py:173-214); the level loop of fmg_solve.
   void enqueue(const T* forcing, T* solution, cudaStream_t s) {
     const int m0 = d.m0, m = d.m;
-    n_launch = 0;
-    n_visit = 0;
-    for (int l = m0; l <= m; l++) lv[l].cur = 0;
-    if (cnt_bytes) {
-      check_cuda(cudaMemsetAsync(cnt_all, 0, cnt_bytes, s), "counter reset");
-      n_launch++;
-    }
-    // f cascade (cycles.py:178-180): up to 6 levels per launch
-    mark_begin(s, m, VK_CASCADE);
-    for (int k = m - 1; k >= m0;) {
-      CascadeDst<T> cd;
-      const int src_l = k + 1;
-      const T* src = (src_l == m) ? forcing : lv[src_l].f;
-      while (cd.levels < 6 && k >= m0) cd.p[cd.levels++] = lv[k--].f;
-      launch_cascade(src, (i64)1 << src_l, cd, d.ld, (int)d.B, s);
-      n_launch++;
-    }
-    mark_end(s);
-    n_visit--;  // the cascade is not a level visit
+    reset_state(s);
     if (use_coarse) {
       enqueue_coarse(forcing, solution, s);
       return;
     }
+    // f cascade (cycles.py:178-180): up to 6 levels per launch
+    mark_begin(s, m, VK_CASCADE);
+    cascade(forcing, m, m0, false, s);
+    mark_end(s);
+    n_visit--;  // the cascade is not a level visit
     visit_direct(s);  // cycles.py:183
     for (int k = m0; k < m; k++) {
       const int t = k + 1;
@@ -500,34 +588,201 @@ struct Plan : PlanBase {
     return a;
   }
 
-  // Schedule with levels m0..Lc resident in one CTA per column group: one
-  // launch for FMG steps m0+1..Lc, then per step t > Lc the grid visits of
-  // levels > Lc around one coarse launch for the V-cycle below Lc+1.
-  void enqueue_coarse(const T* forcing, T* solution, cudaStream_t s) {
-    const int m = d.m;
-    {
-      mark_begin(s, Lc, VK_COARSE);
-      CoarseArgs<T> a = coarse_args(0);
-      a.u_top = lv[Lc].u[lv[Lc].cur];
-      launch_coarse(a, s);
-      n_launch++;
-      mark_end(s);
+  // ---- step schedule (coarse path; the only path that can be sharded) -----------
+  // Levels m0..Lc resident in one CTA per column group: one launch for FMG
+  // steps m0+1..Lc, then per step t > Lc the grid visits of levels > Lc around
+  // one coarse launch for the V-cycle below Lc+1.
+  enum StepKind { ST_LOADF, ST_CASCADE_HI, ST_CASCADE_LO, ST_COARSE_FMG, ST_TOP, ST_DOWN,
+                  ST_COARSE_V, ST_UP };
+  struct Step {
+    int kind, l, t;
+  };
+  std::vector<Step> steps() const {
+    std::vector<Step> st;
+    if (S > 1) {
+      st.push_back({ST_LOADF, d.m, 0});
+      st.push_back({ST_CASCADE_HI, d.m, 0});
     }
-    for (int t = Lc + 1; t <= m; t++) {
-      const T* ft = (t == m) ? forcing : lv[t].f;
-      visit_top(t, ft, s);
-      for (int l = t - 1; l > Lc; l--) visit_down(l, s);
-      mark_begin(s, Lc, VK_COARSE);
-      CoarseArgs<T> a = coarse_args(1);
-      a.u_top = lv[Lc].u[lv[Lc].cur];  // restricted u_{Lc} in, V-cycled u_{Lc} out (in place)
-      a.f_top = lv[Lc].f;
-      launch_coarse(a, s);
-      n_launch++;
-      mark_end(s);
-      for (int l = Lc + 1; l <= t; l++) {
-        const T* fl = (l == m) ? forcing : lv[l].f;
-        visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s);
+    st.push_back({ST_CASCADE_LO, d.m, 0});
+    st.push_back({ST_COARSE_FMG, Lc, 0});
+    for (int t = Lc + 1; t <= d.m; t++) {
+      st.push_back({ST_TOP, t, t});
+      for (int l = t - 1; l > Lc; l--) st.push_back({ST_DOWN, l, t});
+      st.push_back({ST_COARSE_V, Lc, t});
+      for (int l = Lc + 1; l <= t; l++) st.push_back({ST_UP, l, t});
+    }
+    return st;
+  }
+  const T* ffine(const T* forcing) const { return S > 1 ? fm : forcing; }
+  const T* flev(int l, const T* forcing) const { return l == d.m ? ffine(forcing) : lv[l].f; }
+
+  void cascade(const T* src, int src_l, int lo_l, bool slab, cudaStream_t s) {
+    // restrict levels src_l-1 .. lo_l, up to 6 per launch; slab: this shard's rows
+    for (int k = src_l - 1; k >= lo_l;) {
+      CascadeDst<T> cd;
+      const int sl = k + 1;
+      const T* sp = (sl == src_l) ? src : lv[sl].f;
+      const i64 r0 = slab ? c0(sl) : 0, nr = slab ? c1(sl) - c0(sl) : lv[sl].n;
+      while (cd.levels < 6 && k >= lo_l) {
+        cd.p[cd.levels++] = lv[k].f + (slab ? c0(k) : 0) * d.ld;
+        k--;
       }
+      launch_cascade(sp + r0 * d.ld, nr, cd, d.ld, (int)d.B, s);
+      n_launch++;
+    }
+  }
+
+  void run_step(const Step& st, const T* forcing, T* solution, cudaStream_t s) {
+    switch (st.kind) {
+      case ST_LOADF:  // the caller's forcing slab into the halo'd finest buffer
+        check_cuda(cudaMemcpyAsync(fm + c0(d.m) * d.ld, forcing,
+                                   (size_t)(c1(d.m) - c0(d.m)) * d.ld * sizeof(T),
+                                   cudaMemcpyDeviceToDevice, s),
+                   "forcing slab copy");
+        break;
+      case ST_CASCADE_HI:  // this shard's slab, finest level down to Lr
+        mark_begin(s, d.m, VK_CASCADE);
+        cascade(fm, d.m, Lr, true, s);
+        mark_end(s);
+        n_visit--;
+        break;
+      case ST_CASCADE_LO: {  // f cascade (cycles.py:178-180) on replicated levels
+        const int top = S > 1 ? Lr : d.m;
+        mark_begin(s, top, VK_CASCADE);
+        cascade(top == d.m ? forcing : lv[top].f, top, d.m0, false, s);
+        mark_end(s);
+        n_visit--;
+        break;
+      }
+      case ST_COARSE_FMG: {
+        mark_begin(s, Lc, VK_COARSE);
+        CoarseArgs<T> a = coarse_args(0);
+        a.u_top = lv[Lc].u[lv[Lc].cur];
+        launch_coarse(a, s);
+        n_launch++;
+        mark_end(s);
+        break;
+      }
+      case ST_TOP:
+        visit_top(st.l, flev(st.l, forcing), s);
+        break;
+      case ST_DOWN:
+        visit_down(st.l, s);
+        break;
+      case ST_COARSE_V: {
+        mark_begin(s, Lc, VK_COARSE);
+        CoarseArgs<T> a = coarse_args(1);
+        a.u_top = lv[Lc].u[lv[Lc].cur];  // restricted u_{Lc} in, V-cycled u_{Lc} out (in place)
+        a.f_top = lv[Lc].f;
+        launch_coarse(a, s);
+        n_launch++;
+        mark_end(s);
+        break;
+      }
+      case ST_UP: {
+        const bool fin = st.l == d.m && st.t == d.m;
+        T* dst = fin ? (S > 1 ? solution - c0(d.m) * d.ld : solution) : nullptr;
+        visit_up(st.l, flev(st.l, forcing), dst, s);
+        break;
+      }
+    }
+  }
+
+  // ---- communication after a step (sharded plans) ---------------------------------
+  void halo(T* X, int l, int id, std::vector<Xfer>& xs) const {
+    const size_t bytes = (size_t)H * d.ld * sizeof(T);
+    const i64 a = c0(l), b = c1(l);
+    if (srank > 0) {
+      xs.push_back({srank - 1, true, X + a * d.ld, bytes, 2 * id});
+      xs.push_back({srank - 1, false, X + (a - H) * d.ld, bytes, 2 * id + 1});
+    }
+    if (srank < S - 1) {
+      xs.push_back({srank + 1, true, X + (b - H) * d.ld, bytes, 2 * id + 1});
+      xs.push_back({srank + 1, false, X + b * d.ld, bytes, 2 * id});
+    }
+  }
+  void records(int l, std::vector<Xfer>& xs) const {
+    const i64 slot = 5 * ((d.B + 31) / 32) * 32;
+    const size_t bytes = (size_t)slot * sizeof(T);
+    if (srank > 0) {
+      xs.push_back({srank - 1, true, ob[l], bytes, 0});
+      xs.push_back({srank - 1, false, ib[l], bytes, 1});
+    }
+    if (srank < S - 1) {
+      xs.push_back({srank + 1, true, ob[l] + slot, bytes, 1});
+      xs.push_back({srank + 1, false, ib[l] + slot, bytes, 0});
+    }
+  }
+  // transfers, slab-edge fix-ups and all-gathers owed after step st
+  void comm_plan(const Step& st, std::vector<Xfer>& xs, std::vector<Gather>& gs) const {
+    auto gather = [&](T* X, int l) {
+      gs.push_back({(char*)X, (size_t)(lv[l].n / S) * d.ld * sizeof(T)});
+    };
+    switch (st.kind) {
+      case ST_LOADF:
+        halo(fm, d.m, 1, xs);
+        break;
+      case ST_CASCADE_HI:
+        for (int l = Lr + 1; l < d.m; l++) halo(lv[l].f, l, l, xs);
+        gather(lv[Lr].f, Lr);
+        break;
+      case ST_TOP:
+      case ST_DOWN: {
+        const int l = st.l;
+        if (!sharded(l)) break;
+        records(l, xs);
+        if (!is_sr(l)) halo(lv[l].u[lv[l].cur], l, 1, xs);
+        if (sharded(l - 1)) {
+          halo(lv[l - 1].u[lv[l - 1].cur], l - 1, 2, xs);
+          halo(lv[l - 1].f, l - 1, 3, xs);
+        } else if (l - 1 == Lr) {
+          gather(lv[Lr].u[lv[Lr].cur], Lr);
+          gather(lv[Lr].f, Lr);
+        }
+        break;
+      }
+      case ST_UP:
+        if (sharded(st.l) && !(st.l == d.m && st.t == d.m))
+          halo(lv[st.l].u[lv[st.l].cur], st.l, 1, xs);
+        break;
+      default:
+        break;
+    }
+  }
+  // the two coarse cells at each slab boundary of an epilogue visit, from the
+  // own outbox record and the neighbour's record in the inbox
+  void fixup(const Step& st, cudaStream_t s) {
+    if (!(st.kind == ST_TOP || st.kind == ST_DOWN) || !sharded(st.l)) return;
+    const int l = st.l;
+    const i64 slot = 5 * ((d.B + 31) / 32) * 32;
+    T* fH = lv[l - 1].f;
+    if (c0(l) > 0) {
+      launch_edge_fix(ib[l], ob[l], fH, c0(l), lv[l].n, d.ld, (int)d.B, 2, s);
+      n_launch++;
+    }
+    if (c1(l) < lv[l].n) {
+      launch_edge_fix(ob[l] + slot, ib[l] + slot, fH, c1(l), lv[l].n, d.ld, (int)d.B, 2, s);
+      n_launch++;
+    }
+  }
+  NcclApi* nccl = nullptr;
+  void* ncomm = nullptr;
+  void comm_nccl(const Step& st, cudaStream_t s);  // defined after NcclApi
+
+  void reset_state(cudaStream_t s) {
+    n_launch = 0;
+    n_visit = 0;
+    for (int l = d.m0; l <= d.m; l++) lv[l].cur = 0;
+    if (cnt_bytes) {
+      check_cuda(cudaMemsetAsync(cnt_all, 0, cnt_bytes, s), "counter reset");
+      n_launch++;
+    }
+  }
+
+  void enqueue_coarse(const T* forcing, T* solution, cudaStream_t s) {
+    for (const Step& st : steps()) {
+      run_step(st, forcing, solution, s);
+      if (S > 1) comm_nccl(st, s);
     }
   }
 
@@ -619,6 +874,159 @@ struct Plan : PlanBase {
     inf->finest_visit_alg_bytes = words_visit(VK_UP, m) * (double)d.B * sizeof(T);
     inf->coarse_cutoff = use_coarse ? Lc : -1;
     inf->coarse_columns = use_coarse ? CW : 0;
+  }
+};
+
+// ---- NCCL, loaded on demand (libnccl.so.2: torch's copy if already loaded) ----------
+struct NcclApi {
+  typedef int (*GetUniqueId_t)(void*);
+  typedef int (*CommInitRank_t)(void**, int, ncclUniqueId, int);
+  typedef int (*CommDestroy_t)(void*);
+  typedef int (*Group_t)();
+  typedef int (*P2P_t)(const void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*Recv_t)(void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*AllGather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
+  typedef const char* (*ErrStr_t)(int);
+  GetUniqueId_t getUniqueId = nullptr;
+  CommInitRank_t commInitRank = nullptr;
+  CommDestroy_t commDestroy = nullptr;
+  Group_t groupStart = nullptr, groupEnd = nullptr;
+  P2P_t send = nullptr;
+  Recv_t recv = nullptr;
+  AllGather_t allGather = nullptr;
+  ErrStr_t errStr = nullptr;
+  static NcclApi* get() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+      tried = true;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (h) {
+        api.getUniqueId = (GetUniqueId_t)dlsym(h, "ncclGetUniqueId");
+        api.commInitRank = (CommInitRank_t)dlsym(h, "ncclCommInitRank");
+        api.commDestroy = (CommDestroy_t)dlsym(h, "ncclCommDestroy");
+        api.groupStart = (Group_t)dlsym(h, "ncclGroupStart");
+        api.groupEnd = (Group_t)dlsym(h, "ncclGroupEnd");
+        api.send = (P2P_t)dlsym(h, "ncclSend");
+        api.recv = (Recv_t)dlsym(h, "ncclRecv");
+        api.allGather = (AllGather_t)dlsym(h, "ncclAllGather");
+        api.errStr = (ErrStr_t)dlsym(h, "ncclGetErrorString");
+      }
+    }
+    require(api.commInitRank && api.send && api.allGather, "NCCL (libnccl.so.2) not available");
+    return &api;
+  }
+  void check(int rc, const char* what) const {
+    if (rc != 0) throw Error(ERR_CUDA, std::string(what) + ": " + (errStr ? errStr(rc) : "nccl error"));
+  }
+};
+
+// One shard per GPU: transfers become one grouped ncclSend/ncclRecv round,
+// then the slab-edge fix-ups, then in-place ncclAllGather of the cutoff level.
+template <typename T>
+void Plan<T>::comm_nccl(const Step& st, cudaStream_t s) {
+  std::vector<Xfer> xs;
+  std::vector<Gather> gs;
+  comm_plan(st, xs, gs);
+  if (!xs.empty()) {
+    nccl->check(nccl->groupStart(), "ncclGroupStart");
+    for (const Xfer& x : xs) {
+      if (x.send) nccl->check(nccl->send(x.ptr, x.bytes, ncclUint8, x.peer, ncomm, s), "ncclSend");
+      else nccl->check(nccl->recv(x.ptr, x.bytes, ncclUint8, x.peer, ncomm, s), "ncclRecv");
+    }
+    nccl->check(nccl->groupEnd(), "ncclGroupEnd");
+  }
+  fixup(st, s);
+  for (const Gather& g : gs)
+    nccl->check(nccl->allGather(g.base + srank * g.chunk, g.base, g.chunk, ncclUint8, ncomm, s),
+                "ncclAllGather");
+}
+
+// Virtual shards: S plans of one problem on one device, run in lockstep on one
+// stream; the transfers between them are device copies.  Exercises exactly the
+// sharded schedule, halos, edge records and cutoff gather of the NCCL path,
+// bit-exact against the unsharded solve (tests/test_gpu_shard.py).
+struct GroupBase {
+  virtual ~GroupBase() {}
+  virtual void solve(const void* in, void* out, cudaStream_t s) = 0;
+  virtual int cutoff() const = 0;
+  virtual i64 halo_rows() const = 0;
+};
+
+template <typename T>
+struct ShardGroup : GroupBase {
+  std::vector<std::unique_ptr<Plan<T>>> sh;
+  cudaStream_t cap = nullptr;
+  std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
+  bool use_graph;
+  ShardGroup(const fmgsr_plan_desc& d, int S) : use_graph(d.use_graph != 0) {
+    for (int k = 0; k < S; k++) sh.emplace_back(new Plan<T>(d, S, k));
+    check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "group stream");
+  }
+  ~ShardGroup() override {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (cap) cudaStreamDestroy(cap);
+  }
+  int cutoff() const override { return sh[0]->Lr; }
+  i64 halo_rows() const override { return sh[0]->H; }
+  void enqueue(const T* forcing, T* sol, cudaStream_t s) {
+    const int S = (int)sh.size();
+    const i64 ld = sh[0]->d.ld;
+    for (auto& p : sh) p->reset_state(s);
+    for (const auto& st : sh[0]->steps()) {
+      std::vector<std::vector<Xfer>> xs(S);
+      std::vector<std::vector<Gather>> gs(S);
+      for (int k = 0; k < S; k++) {
+        const i64 r0 = sh[k]->c0(sh[k]->d.m);
+        sh[k]->run_step(st, forcing + r0 * ld, sol + r0 * ld, s);
+      }
+      for (int k = 0; k < S; k++) sh[k]->comm_plan(st, xs[k], gs[k]);
+      for (int k = 0; k < S; k++)  // each send lands in the peer's matching receive
+        for (const Xfer& x : xs[k]) {
+          if (!x.send) continue;
+          const Xfer* r = nullptr;
+          for (const Xfer& y : xs[x.peer])
+            if (!y.send && y.peer == k && y.tag == x.tag && y.bytes == x.bytes) r = &y;
+          require(r != nullptr, "shard group: unmatched transfer");
+          check_cuda(cudaMemcpyAsync(r->ptr, x.ptr, x.bytes, cudaMemcpyDeviceToDevice, s), "xfer");
+        }
+      for (int k = 0; k < S; k++) sh[k]->fixup(st, s);
+      for (int k = 0; k < S; k++)
+        for (size_t g = 0; g < gs[k].size(); g++)
+          for (int j = 0; j < S; j++)
+            if (j != k)
+              check_cuda(cudaMemcpyAsync(gs[j][g].base + k * gs[k][g].chunk,
+                                         gs[k][g].base + k * gs[k][g].chunk, gs[k][g].chunk,
+                                         cudaMemcpyDeviceToDevice, s),
+                         "gather");
+    }
+  }
+  void solve(const void* in, void* out, cudaStream_t s) override {
+    const T* f = (const T*)in;
+    T* u = (T*)out;
+    if (!use_graph) {
+      enqueue(f, u, s);
+      return;
+    }
+    auto key = std::make_pair(in, out);
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+      cudaGraph_t g;
+      check_cuda(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue(f, u, cap);
+      } catch (...) {
+        cudaStreamEndCapture(cap, &g);
+        throw;
+      }
+      check_cuda(cudaStreamEndCapture(cap, &g), "end capture");
+      cudaGraphExec_t ex;
+      check_cuda(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+      cudaGraphDestroy(g);
+      it = graphs.emplace(key, ex).first;
+    }
+    check_cuda(cudaGraphLaunch(it->second, s), "graph launch");
   }
 };
 
@@ -878,6 +1286,65 @@ int fmgsr_fourier_rhs_f32(const double* coef, int K, int64_t n, int64_t B, int64
 }
 
 // ---- plan ------------------------------------------------------------------------
+int fmgsr_nccl_unique_id(void* id) {
+  return guarded([&] {
+    require(id != nullptr, "nccl_unique_id: null argument");
+    NcclApi* api = NcclApi::get();
+    require(api->getUniqueId != nullptr, "ncclGetUniqueId missing");
+    api->check(api->getUniqueId(id), "ncclGetUniqueId");
+  });
+}
+int fmgsr_shard_plan_create(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                            const void* nccl_id, void** plan) {
+  return guarded([&] {
+    require(desc && plan && nccl_id, "shard_plan_create: null argument");
+    validate_desc(*desc);
+    require(shards >= 2 && rank >= 0 && rank < shards, "shard_plan_create: bad rank / shards");
+    NcclApi* api = NcclApi::get();
+    ncclUniqueId uid;
+    std::memcpy(&uid, nccl_id, sizeof uid);
+    void* comm = nullptr;
+    api->check(api->commInitRank(&comm, shards, uid, rank), "ncclCommInitRank");
+    PlanBase* p;
+    if (desc->dtype == 0) {
+      auto* q = new Plan<double>(*desc, shards, rank);
+      q->nccl = api;
+      q->ncomm = comm;
+      p = q;
+    } else {
+      auto* q = new Plan<float>(*desc, shards, rank);
+      q->nccl = api;
+      q->ncomm = comm;
+      p = q;
+    }
+    *plan = p;
+  });
+}
+int fmgsr_shard_group_create(const fmgsr_plan_desc* desc, int32_t shards, void** group) {
+  return guarded([&] {
+    require(desc && group, "shard_group_create: null argument");
+    validate_desc(*desc);
+    require(shards >= 2, "shard_group_create: need >= 2 shards");
+    if (desc->dtype == 0) *group = new ShardGroup<double>(*desc, shards);
+    else *group = new ShardGroup<float>(*desc, shards);
+  });
+}
+int fmgsr_shard_group_solve(void* group, const void* forcing, void* solution, void* stream) {
+  return guarded([&] {
+    require(group && forcing && solution, "shard_group_solve: null argument");
+    reinterpret_cast<GroupBase*>(group)->solve(forcing, solution, S(stream));
+  });
+}
+int fmgsr_shard_group_cutoff(void* group, int32_t* cutoff, int64_t* halo_rows) {
+  return guarded([&] {
+    require(group && cutoff && halo_rows, "shard_group_cutoff: null argument");
+    *cutoff = reinterpret_cast<GroupBase*>(group)->cutoff();
+    *halo_rows = reinterpret_cast<GroupBase*>(group)->halo_rows();
+  });
+}
+int fmgsr_shard_group_destroy(void* group) {
+  return guarded([&] { delete reinterpret_cast<GroupBase*>(group); });
+}
 int fmgsr_plan_create(const fmgsr_plan_desc* desc, void** plan) {
   return guarded([&] {
     require(desc && plan, "plan_create: null argument");

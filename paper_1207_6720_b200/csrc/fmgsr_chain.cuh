@@ -182,7 +182,7 @@ struct Chain {
       lo = lo > a ? lo : a;
       hi = hi < b ? hi : b;
     }
-    hi = hi < nc - 3 - D ? hi : nc - 3 - D;
+    hi = hi < src.qhi - 2 - D ? hi : src.qhi - 2 - D;  // unclamped fast issue stays in memory
     const i64 oq = os >> 1;
     i64 q = qs;
     // buffer cells left of the owned range

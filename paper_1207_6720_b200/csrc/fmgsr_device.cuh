@@ -203,12 +203,13 @@ struct PairSource {
   i64 ld, nc;   // row stride, number of pairs (= coarse cells)
   KzCoef<T> kz;
   i64 wlo, whi;  // Kaczmarz pair range
+  i64 qlo, qhi;  // pairs that exist in memory (the whole level, or a shard's slab + halo)
   T s0, s1, s2, s3;
   // fast-issue row pointers (pair g): f row 2g, u row (LOAD 2g | CORR 2g+2),
   // uH row (CORR g+1 | FMG g+2), uc row g
   const T *pf, *pu, *ph, *pc;
 
-  __device__ __forceinline__ i64 cl(i64 q) const { return q < 0 ? 0 : (q >= nc ? nc - 1 : q); }
+  __device__ __forceinline__ i64 cl(i64 q) const { return q < qlo ? qlo : (q > qhi ? qhi : q); }
 
   // slot layout: sl[k * NT] for k < R (NT = threads per block)
   template <int NT>

@@ -33,7 +33,7 @@ inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(ERR_ARG, msg);
 }
 
-inline int level_of(i64 n) {
+__host__ __device__ inline int level_of(i64 n) {
   int k = 0;
   while (((i64)1 << (k + 1)) <= n) k++;
   return k;
@@ -117,7 +117,22 @@ struct VisitDesc {
   const i64* elo = nullptr;
   const i64* ehi = nullptr;
   i64 P = 0;  // number of patches when arrays are given
+  // patch-slab sharding (uniform geometry): patches [p_begin, p_begin + p_count)
+  // of the level, pair loads clamped to [qlo, qhi] (the slab and its halo;
+  // -1: the whole level).  Edge records of the slab's outer boundaries go to
+  // E_out[slot][5][Bpad] (slot 0: left edge, 1: right edge) instead of the
+  // in-kernel last-arriver protocol when left_remote / right_remote.
+  i64 p_begin = 0, p_count = -1;
+  i64 qlo = -1, qhi = -1;
+  T* E_out = nullptr;
+  bool left_remote = false, right_remote = false;
 };
+
+// Complete the owned coarse cell at a shard's slab boundary from the two edge
+// records (own outbox slot, neighbour's record received in the inbox).
+template <typename T>
+void launch_edge_fix(const T* rec_left, const T* rec_right, T* fH, i64 s, i64 nf, i64 ld, int B,
+                     int which, cudaStream_t st);
 
 template <typename T>
 void launch_visit(const VisitDesc<T>& d, cudaStream_t s);

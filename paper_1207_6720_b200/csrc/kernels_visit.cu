@@ -21,7 +21,9 @@ namespace fmgsr {
 
 template <typename T>
 struct VisitArgs {
-  i64 n, ld, W, b, P, nc;
+  i64 n, ld, W, b, P, nc, p_begin, qlo, qhi;
+  T* E_out;
+  bool left_remote, right_remote;
   int B, nrg;
   GsCoef<T> gc;
   KzCoef<T> kz;
@@ -50,9 +52,10 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 p = gw / a.nrg;
-  const int rg = (int)(gw - p * a.nrg);
-  if (p >= a.P) return;  // warp-uniform
+  const i64 pl = gw / a.nrg;  // patch index within the launched range
+  const int rg = (int)(gw - pl * a.nrg);
+  if (pl >= a.P) return;  // warp-uniform
+  const i64 p = a.p_begin + pl;
   const int r = rg * 32 + lane;
   const bool store = r < a.B;
   const int rr = store ? r : a.B - 1;
@@ -89,6 +92,8 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
   ch.src.kz = a.kz;
   ch.src.wlo = ws >> 1;
   ch.src.whi = we >> 1;
+  ch.src.qlo = a.qlo;
+  ch.src.qhi = a.qhi;
   ch.gc = a.gc;
   ch.n = a.n;
   ch.nc = a.nc;
@@ -121,12 +126,24 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
   EdgeRec<T> right;
   ep.finish(store, right);
   const i64 ldE = (i64)a.nrg * 32;
-  if (!ep.left_dom)
-    edge_arrive(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, a.ld, os,
-                ep.inv_h2, ep.inv_H2);
-  if (!ep.right_dom)
-    edge_arrive(a.E, a.cnt, ldE, a.nrg, p + 1, 0, right, lane, rg, r, store, ep.fH_out, a.ld, oe,
-                ep.inv_h2, ep.inv_H2);
+  if (!ep.left_dom) {
+    if (pl == 0 && a.left_remote) {  // slab edge: the neighbour shard finishes it
+#pragma unroll
+      for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = ep.left.v[k];
+    } else {
+      edge_arrive(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, a.ld, os,
+                  ep.inv_h2, ep.inv_H2);
+    }
+  }
+  if (!ep.right_dom) {
+    if (pl == a.P - 1 && a.right_remote) {
+#pragma unroll
+      for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
+    } else {
+      edge_arrive(a.E, a.cnt, ldE, a.nrg, p + 1, 0, right, lane, rg, r, store, ep.fH_out, a.ld, oe,
+                  ep.inv_h2, ep.inv_H2);
+    }
+  }
 }
 
 template <typename T>
@@ -229,6 +246,12 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   a.ohi = d.ohi;
   a.elo = d.elo;
   a.ehi = d.ehi;
+  a.p_begin = 0;
+  a.qlo = d.qlo >= 0 ? d.qlo : 0;
+  a.qhi = d.qhi >= 0 ? d.qhi : a.nc - 1;
+  a.E_out = d.E_out;
+  a.left_remote = d.left_remote;
+  a.right_remote = d.right_remote;
   if (d.olo) {
     require(d.src == SRC_LOAD && !d.epi, "visit: patch arrays only with plain loads");
     a.P = d.P;
@@ -240,7 +263,13 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
     a.W = d.W;
     a.b = d.b;
     a.P = d.n / d.W;
+    if (d.p_count >= 0) {
+      require(d.p_begin >= 0 && d.p_begin + d.p_count <= a.P, "visit: patch range outside the level");
+      a.p_begin = d.p_begin;
+      a.P = d.p_count;
+    }
   }
+  require(!(d.left_remote || d.right_remote) || (d.E_out && d.epi), "visit: remote edges need an outbox");
   if (d.src == SRC_LOAD) require(d.u_src != nullptr, "visit: LOAD needs u_src");
   if (d.src == SRC_CORR) require(d.u_src && d.uH, "visit: CORR needs u_src and uH");
   if (d.src == SRC_FMG) require(d.uH && d.n >= 8, "visit: FMG needs uH with >= 4 coarse cells");
@@ -410,6 +439,37 @@ void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s) {
   }
   check_launch("smooth_scratch_kernel");
 }
+
+// Slab-boundary coarse cell (which = 0: s/2 - 1, owned by the left shard;
+// which = 1: s/2, owned by the right shard) from the two edge records.
+template <typename T>
+__global__ void k_edge_fix(const T* __restrict__ L, const T* __restrict__ R, T* fH, i64 s, i64 nf,
+                           i64 ld, int B, i64 ldE, int which) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  const int lv = level_of(nf);
+  const T ih = (T)(double)((i64)1 << (2 * lv)), iH = (T)(double)((i64)1 << (2 * (lv - 1)));
+  T Lr[5], Rr[5];
+#pragma unroll
+  for (int k = 0; k < 5; k++) {
+    Lr[k] = L[k * ldE + r];
+    Rr[k] = R[k * ldE + r];
+  }
+  T fL, fR;
+  edge_finish(Lr, Rr, ih, iH, fL, fR);
+  if (which != 1) fH[(s / 2 - 1) * ld + r] = fL;  // 0: left cell, 1: right cell, 2: both
+  if (which != 0) fH[(s / 2) * ld + r] = fR;
+}
+
+template <typename T>
+void launch_edge_fix(const T* rec_left, const T* rec_right, T* fH, i64 s, i64 nf, i64 ld, int B,
+                     int which, cudaStream_t st) {
+  const i64 ldE = ((B + 31) / 32) * 32;
+  k_edge_fix<T><<<(B + 127) / 128, 128, 0, st>>>(rec_left, rec_right, fH, s, nf, ld, B, ldE, which);
+  check_launch("edge_fix");
+}
+template void launch_edge_fix<double>(const double*, const double*, double*, i64, i64, i64, int, int, cudaStream_t);
+template void launch_edge_fix<float>(const float*, const float*, float*, i64, i64, i64, int, int, cudaStream_t);
 
 template void launch_visit<double>(const VisitDesc<double>&, cudaStream_t);
 template void launch_visit<float>(const VisitDesc<float>&, cudaStream_t);

@@ -1,0 +1,127 @@
+"""Patch-slab sharding of one FMG-FAS-SR solve.
+
+The finest levels are split into S contiguous slabs of patches (the additive
+smoother makes patches independent; only stencil halos and the tau edge
+records at slab boundaries couple neighbours); levels at or below the
+replication cutoff are all-gathered once per V-cycle and solved redundantly
+by every shard.  Two drivers run the same sharded schedule:
+
+* ``ShardGroup``: S virtual shards on the current device, in lockstep on one
+  stream, transfers as device copies -- bit-identical to the unsharded plan
+  (``tests/test_gpu_shard.py``);
+* ``ShardedPlan``: one shard per GPU (one process per GPU, torchrun), halos
+  and edge records over NCCL send/recv, the cutoff level over NCCL all-gather,
+  all captured in the plan's CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from .plan import PlanKey, key_from_config
+
+
+def _desc(key: PlanKey) -> N.PlanDesc:
+    d = N.PlanDesc()
+    d.m0, d.m, d.n_sr, d.ns = key.m0, key.m, key.n_sr, key.ns
+    d.geom_mode = key.geom_mode
+    d.dtype = 0 if key.dtype == torch.float64 else 1
+    d.P, d.b, d.B, d.ld = key.P, key.b, key.B, key.B
+    d.omega = key.omega
+    d.fused = int(key.fused)
+    d.use_graph = int(key.use_graph)
+    d.coarse = int(key.coarse)
+    d.nonlinear = int(key.nonlinear)
+    return d
+
+
+def slab(n: int, shards: int, rank: int) -> tuple[int, int]:
+    """Rows [c0, c1) of an n-cell level owned by ``rank``."""
+    w = n // shards
+    return rank * w, (rank + 1) * w
+
+
+class ShardGroup:
+    """All ``shards`` slabs of one problem on this device (virtual shards)."""
+
+    def __init__(self, cfg, B: int, shards: int, dtype=torch.float64, coarse: int = -1,
+                 use_graph: bool = True):
+        N.require_cuda()
+        self.key = key_from_config(cfg, B, dtype, use_graph=use_graph, coarse=coarse)
+        d = _desc(self.key)
+        h = C.c_void_p()
+        N.check(N.lib().fmgsr_shard_group_create(C.byref(d), int(shards), C.byref(h)),
+                "shard_group_create")
+        self._h = h
+        self.shards = shards
+        self.N = 2 ** self.key.m
+        cut, halo = C.c_int32(), C.c_int64()
+        N.check(N.lib().fmgsr_shard_group_cutoff(h, C.byref(cut), C.byref(halo)), "cutoff")
+        self.cutoff, self.halo = cut.value, halo.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.lib().fmgsr_shard_group_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def solve(self, forcing: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty_like(forcing)
+        k = self.key
+        for t in (forcing, out):
+            if not t.is_cuda or t.dtype != k.dtype or tuple(t.shape) != (self.N, k.B) \
+                    or not t.is_contiguous():
+                raise ValueError(f"expected a contiguous CUDA {k.dtype} tensor ({self.N}, {k.B})")
+        N.check(N.lib().fmgsr_shard_group_solve(self._h, forcing.data_ptr(), out.data_ptr(),
+                                                N.stream_ptr()), "shard_group_solve")
+        return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    N.check(N.lib().fmgsr_nccl_unique_id(buf), "nccl_unique_id")
+    return bytes(buf)
+
+
+class ShardedPlan:
+    """This rank's shard of one problem, one GPU per rank, exchanges over NCCL.
+
+    ``uid`` is the 128-byte id from ``nccl_unique_id()`` on rank 0, broadcast
+    to every rank (e.g. with torch.distributed).  ``solve`` takes and returns
+    the rank's slab: (2**m / shards, B) rows [c0, c1) of the global arrays."""
+
+    def __init__(self, cfg, B: int, shards: int, rank: int, uid: bytes, dtype=torch.float64,
+                 coarse: int = -1, use_graph: bool = True):
+        N.require_cuda()
+        self.key = key_from_config(cfg, B, dtype, use_graph=use_graph, coarse=coarse)
+        d = _desc(self.key)
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        N.check(N.lib().fmgsr_shard_plan_create(C.byref(d), int(shards), int(rank), idbuf,
+                                                C.byref(h)), "shard_plan_create")
+        self._h = h
+        self.shards, self.rank = shards, rank
+        self.rows = 2 ** self.key.m // shards
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.lib().fmgsr_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def solve(self, forcing_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty_like(forcing_slab)
+        N.check(N.lib().fmgsr_plan_solve(self._h, forcing_slab.data_ptr(), out.data_ptr(),
+                                         N.stream_ptr()), "plan_solve")
+        return out
