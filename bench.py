@@ -359,6 +359,102 @@ def run_gpu(args, w):
     return 0
 
 
+def run_gpu_sharded(args, w):
+    """One problem split across the ranks by patch slabs: strong
+    scaling (total work fixed), halos / tau edge records over NCCL send/recv,
+    the replication cutoff level over NCCL all-gather."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1207_6720_b200 as fm
+    from paper_1207_6720_b200.shard import ShardedPlan, nccl_unique_id, slab
+
+    world, rank, local = dist_env()
+    if world == 1:
+        return run_gpu(args, w)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = torch.float64 if w["dtype"] == "f64" else torch.float32
+    m, B = w["m"], w["B"]
+    n = 2 ** m
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], m), n_sr=w["n_sr"],
+                          smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    plan = ShardedPlan(cfg, B, world, rank, bytes(uid.cpu().numpy().tobytes()), dtype)
+    f, _ = fm.fourier_batch(n, fm.fourier_coefficients(B, seed=0), dtype, with_exact=False)
+    c0, c1 = slab(n, world, rank)
+    fs = f[c0:c1].contiguous()
+    del f
+    sol = torch.empty_like(fs)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.solve(fs, sol)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.solve(fs, sol)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop()
+    ms_step = reduce_max(e0.elapsed_time(e1), world) / args.steps
+    value = B * n / (ms_step / 1e3)  # the whole problem, solved by all ranks together
+    # end to end: this rank's slab from / to pinned host memory
+    hf = fs.cpu().pin_memory()
+    hs = torch.empty_like(hf).pin_memory()
+    dfi = torch.empty_like(fs)
+
+    def e2e_step():
+        dfi.copy_(hf, non_blocking=True)
+        plan.solve(dfi, sol)
+        hs.copy_(sol, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2e_ms = reduce_max(e0.elapsed_time(e1), world) / args.steps
+    esz = 8 if dtype == torch.float64 else 4
+    peak, peak_src = measured_peak()
+    # per-GPU share of the whole cycle's algorithmic bytes (29 words / unknown)
+    alg = 29.0 * n * B * esz
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": w["dtype"], "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
+            "config": dict(workload_config(args.workload, w, 1),
+                           parallelism=f"patch slabs x{world} (NCCL halos, replicated coarse)"),
+            "roofline": {"bound": "hbm", "achieved": alg / world / (ms_step / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": alg / world / (ms_step / 1e3) / 1e9 / peak, "traffic": None,
+                         "kernel": "whole cycle per GPU (29 algorithmic words / unknown)",
+                         "peak_source": peak_src},
+            "e2e": {"value": B * n / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": (c1 - c0) * B * esz * world,
+                    "d2h_bytes_per_step": (c1 - c0) * B * esz * world, "ms_per_step": e2e_ms},
+            "clocks": clocks, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,11 +466,16 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--shard", default="rhs", choices=["rhs", "patches"],
+                    help="multi-GPU split: independent RHS batches per rank (weak), or "
+                         "patch slabs of one problem (strong, SURVEY 8(e))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args, w)
+    if args.shard == "patches":
+        return run_gpu_sharded(args, w)
     return run_gpu(args, w)
 
 
