@@ -144,6 +144,15 @@ int fmgsr_fourier_rhs_f32(const double* coef, int K, int64_t n, int64_t B, int64
 int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* stream);
 int fmgsr_nonlinear_rhs_f32(const double* scale, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* stream);
 
+/* ---- Self-test (not on the solve path) ----------------------------------
+ * The nonlinear smoother divides x / J with a reciprocal of J computed ahead
+ * of the Gauss-Seidel dependency chain plus two Markstein corrections.  This
+ * runs that division on DEVICE arrays x[n], J[n] (q may be NULL) and ADDS to
+ * the DEVICE counter *bad the number of results not bitwise equal to the IEEE
+ * division. */
+int fmgsr_div_check_f64(const double* x, const double* J, double* q, int64_t n, unsigned long long* bad, void* stream);
+int fmgsr_div_check_f32(const float* x, const float* J, float* q, int64_t n, unsigned long long* bad, void* stream);
+
 /* ---- Whole-solve plan: fmg_solve (cycles.py:137-222) -------------------- */
 typedef struct fmgsr_plan_desc {
   int32_t m0, m;      /* hierarchy 2^m0 .. 2^m (cycles.py:39-49 limits) */

@@ -69,6 +69,7 @@ _SIGS = {
     "fmgsr_fourier_rhs": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_nonlinear_rhs": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_smooth_scratch_rows": (_i64, [_i64, _i64, _i64]),
+    "fmgsr_div_check": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fmgsr_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_vp)]),
     "fmgsr_plan_destroy": (C.c_int, [_vp]),
     "fmgsr_plan_get_info": (C.c_int, [_vp, C.POINTER(PlanInfo)]),
@@ -88,7 +89,7 @@ _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmg
           "fmgsr_prolong_fmg", "fmgsr_tau_correction", "fmgsr_coarse_rhs", "fmgsr_fas_correct",
           "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_fourier_rhs",
           "fmgsr_nonlinear_rhs", "fmgsr_smooth_uniform_nl", "fmgsr_coarse_rhs_nl",
-          "fmgsr_direct_solve_nl"}
+          "fmgsr_direct_solve_nl", "fmgsr_div_check"}
 
 _lib = None
 _lock = threading.Lock()

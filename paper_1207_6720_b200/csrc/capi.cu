@@ -357,6 +357,32 @@ struct Plan : PlanBase {
   // fused prologue + ns = 1 chain (linear smoother only)
   bool fused_chain_ok() const { return d.fused && d.ns == 1 && !d.nonlinear; }
 
+  // V(2,2) streaming smoother with the visit prologue fused (kernels_ns2.cu)
+  bool ns2_ok(const Level& L) const { return d.fused && d.ns == 2 && L.n >= 8; }
+  void smooth_ns2(int l, int src, const T* u_src, const T* uH, bool cr, const T* f, T* out,
+                  cudaStream_t s) {
+    const Level& L = lv[l];
+    Ns2Desc<T> c;
+    c.src = src;
+    c.cr = cr;
+    c.nonlinear = d.nonlinear != 0;
+    c.n = L.n;
+    c.ld = d.ld;
+    c.B = (int)d.B;
+    c.W = L.W;
+    c.b = L.b;
+    c.omega = d.omega;
+    c.u_src = u_src;
+    c.uH = uH;
+    c.uc = (cr && src != SRC_FMG) ? uH : nullptr;
+    c.f = f;
+    c.u_out = out;
+    c.scratch = scratch;
+    c.sld = sld;
+    launch_smooth_ns2(c, s);
+    n_launch++;
+  }
+
   void smooth_into(int l, const T* u_in, const T* f, const T* uc, T* out, cudaStream_t s) {
     const Level& L = lv[l];
     if (d.ns == 1 && !d.nonlinear) {
@@ -442,6 +468,11 @@ struct Plan : PlanBase {
       L.cur ^= 1;
       launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s, d.nonlinear != 0);
       n_launch++;
+    } else if (ns2_ok(L)) {
+      smooth_ns2(t, SRC_FMG, nullptr, uH_in, false, ft, L.u[L.cur ^ 1], s);
+      L.cur ^= 1;
+      launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s, d.nonlinear != 0);
+      n_launch++;
     } else {
       launch_prolong_fmg(uH_in, tmp, H.n, d.ld, (int)d.B, s);
       n_launch++;
@@ -483,7 +514,8 @@ struct Plan : PlanBase {
       if (v.write_u) L.cur ^= 1;
       if (v.uH_out) H.cur ^= 1;
     } else {
-      smooth_into(l, L.u[L.cur], L.f, nullptr, L.u[L.cur ^ 1], s);
+      if (ns2_ok(L)) smooth_ns2(l, SRC_LOAD, L.u[L.cur], nullptr, false, L.f, L.u[L.cur ^ 1], s);
+      else smooth_into(l, L.u[L.cur], L.f, nullptr, L.u[L.cur ^ 1], s);
       L.cur ^= 1;
       launch_restrict_tau(L.u[L.cur], L.f, H.u[H.cur ^ 1], H.f, L.n, d.ld, (int)d.B, 2, s,
                           d.nonlinear != 0);
@@ -518,6 +550,8 @@ struct Plan : PlanBase {
       shard_desc(v, l);
       launch_visit(v, s);
       n_launch++;
+    } else if (ns2_ok(L)) {
+      smooth_ns2(l, sr ? SRC_FMG : SRC_CORR, sr ? nullptr : L.u[L.cur], uH, sr, fl, out, s);
     } else {
       if (sr) launch_prolong_fmg(uH, tmp, H.n, d.ld, (int)d.B, s);
       else launch_fas_correct(L.u[L.cur], uH, tmp, L.n, d.ld, (int)d.B, s);
@@ -1277,6 +1311,12 @@ int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t l
 }
 int fmgsr_nonlinear_rhs_f32(const double* scale, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* s) {
   return guarded([&] { check_field(n, B, ld, "nonlinear_rhs"); launch_nonlinear_rhs<float>(scale, n, ld, (int)B, f, uex, S(s)); });
+}
+int fmgsr_div_check_f64(const double* x, const double* J, double* q, int64_t n, unsigned long long* bad, void* s) {
+  return guarded([&] { launch_div_check<double>(x, J, q, n, bad, S(s)); });
+}
+int fmgsr_div_check_f32(const float* x, const float* J, float* q, int64_t n, unsigned long long* bad, void* s) {
+  return guarded([&] { launch_div_check<float>(x, J, q, n, bad, S(s)); });
 }
 int fmgsr_fourier_rhs_f64(const double* coef, int K, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* s) {
   return guarded([&] { check_field(n, B, ld, "fourier_rhs"); launch_fourier_rhs<double>(coef, K, n, ld, (int)B, f, uex, S(s)); });

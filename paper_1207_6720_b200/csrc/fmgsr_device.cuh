@@ -49,6 +49,7 @@ struct GsCoef {
   T rdiag;   // 1 / (2 * 4^k), exact
   T diag_b;  // 3 * 4^k
   T omega;
+  T diag_i;  // 2 * 4^k, exact (interior diagonal)
 };
 
 template <typename T>
@@ -95,6 +96,63 @@ __device__ __forceinline__ T gs_cell_nl(const GsCoef<T>& c, i64 i, i64 n, T uL, 
   T r = xsub(f, xadd(xmul(c.inv_h2, s), xmul(uu, u)));
   T J = xadd(diag, xmul(T(3), uu));
   return xadd(u, xdiv(xmul(c.omega, r), J));
+}
+
+// x / J with y = RN(1/J) computed off the dependency chain.  q0 = RN(x y) is
+// within 1.5 ulp of x/J; one Markstein correction q1 = RN(q0 + (x - J q0) y)
+// makes it faithful, and by Markstein's theorem (y correctly rounded, q
+// faithful, no underflow) the second correction yields RN(x/J), i.e. the
+// __ddiv_rn result.  Outside the range where the theorem's no-underflow /
+// no-overflow conditions hold (and for zeros, NaN, Inf) it falls back to the
+// IEEE division.  tests/test_gpu_nonlinear.py checks it against xdiv.
+__device__ __forceinline__ double xrcp(double J) { return __drcp_rn(J); }
+__device__ __forceinline__ float xrcp(float J) { return __frcp_rn(J); }
+__device__ __forceinline__ double xfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float xfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ bool div_safe(double x, double J) {
+  const int ex = (__double2hiint(x) >> 20) & 0x7ff, eJ = (__double2hiint(J) >> 20) & 0x7ff;
+  return (unsigned)(ex - (1023 - 800)) <= 1600u && (unsigned)(eJ - (1023 - 100)) <= 300u;
+}
+__device__ __forceinline__ bool div_safe(float x, float J) {
+  const int ex = (__float_as_int(x) >> 23) & 0xff, eJ = (__float_as_int(J) >> 23) & 0xff;
+  return (unsigned)(ex - (127 - 40)) <= 80u && (unsigned)(eJ - (127 - 20)) <= 90u;
+}
+// out of line so the compiler cannot if-convert the rare fallback into the
+// fast path (it would evaluate both divisions)
+template <typename T>
+__device__ __noinline__ T div_slow(T x, T J) {
+  return xdiv(x, J);
+}
+template <typename T>
+__device__ __forceinline__ T div_by(T x, T J, T y) {
+  T q = xmul(x, y);
+  T r = xfma(-J, q, x);
+  q = xfma(r, y, q);
+  r = xfma(-J, q, x);
+  q = xfma(r, y, q);
+  if (!div_safe(x, J)) q = div_slow(x, J);
+  return q;
+}
+
+// Interior nonlinear GS cell (gs_cell_nl, i not a domain row) with the
+// division split: J and 1/J depend only on the old u, so they are computed
+// ahead of the uL dependency.
+template <typename T, bool OMEGA1>
+__device__ __forceinline__ T gs_int_nl(const GsCoef<T>& c, T uL, T u, T uR, T f) {
+  T uu = xmul(u, u);
+  T J = xadd(c.diag_i, xmul(T(3), uu));
+  T y = xrcp(J);
+  T s = xsub(xsub(xmul(T(2), u), uL), uR);
+  T r = xsub(f, xadd(xmul(c.inv_h2, s), xmul(uu, u)));
+  T x = OMEGA1 ? r : xmul(c.omega, r);
+  return xadd(u, div_by(x, J, y));
+}
+
+template <typename T, bool OMEGA1>
+__device__ __forceinline__ T gs_int_o(const GsCoef<T>& c, T uL, T u, T uR, T f) {
+  T s = xsub(xsub(xmul(T(2), u), uL), uR);
+  T resid = xsub(f, xmul(c.inv_h2, s));
+  return xadd(u, xmul(OMEGA1 ? resid : xmul(c.omega, resid), c.rdiag));
 }
 
 // Kaczmarz projection of one pair onto its coarse value, reference

@@ -162,6 +162,28 @@ struct ScratchDesc {
 
 template <typename T>
 void launch_smooth_scratch(const ScratchDesc<T>& d, cudaStream_t s);
+
+// ns = 2 (V(2,2)) streaming smoother, uniform geometry: forward chain with the
+// visit prologue, window spilled to scratch, backward chain from the spill.
+template <typename T>
+struct Ns2Desc {
+  int src = 0;  // SRC_LOAD / SRC_CORR / SRC_FMG
+  bool cr = false, nonlinear = false;
+  i64 n = 0, ld = 0;
+  int B = 0;
+  i64 W = 0, b = 0;
+  double omega = 1.0, proj_diag = 0.5;
+  const T* u_src = nullptr;
+  const T* uH = nullptr;
+  const T* uc = nullptr;
+  const T* f = nullptr;
+  T* u_out = nullptr;
+  T* scratch = nullptr;  // (n / W) * (W + 2b + 2) rows of sld
+  i64 sld = 0;
+};
+
+template <typename T>
+void launch_smooth_ns2(const Ns2Desc<T>& d, cudaStream_t s);
 inline i64 scratch_rows_uniform(i64 n, i64 W, i64 b) { return (n / W) * (W + 2 * b + 2); }
 
 // Stencil / level operators ([n][ld] layout, B active columns).
@@ -179,6 +201,7 @@ template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, 
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);
 template <typename T> void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop, double proj_diag, cudaStream_t s);
 template <typename T> void launch_fourier_rhs(const double* coef, int K, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
+template <typename T> void launch_div_check(const T* x, const T* J, T* q, i64 n, unsigned long long* bad, cudaStream_t s);
 template <typename T> void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
 
 }  // namespace fmgsr

@@ -202,6 +202,7 @@ struct CoarseCtx {
     gc.rdiag = (T)pow2d(-(2 * l + 1));
     gc.diag_b = xmul(T(3), gc.inv_h2);
     gc.omega = (T)a.omega;
+    gc.diag_i = xmul(T(2), gc.inv_h2);
     for (int k = threadIdx.x; k < P * CW; k += blockDim.x) {
       const int p = k / CW, c = k % CW;
       const int os = p * W, oe = os + W;

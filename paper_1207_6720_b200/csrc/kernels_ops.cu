@@ -159,6 +159,80 @@ __global__ void k_restrict_tau(const T* __restrict__ u, const T* __restrict__ f,
   }
 }
 
+// The same restriction + tau as a streaming pass: each thread walks a segment
+// of coarse rows of one column with a sliding window (pair j-1, j, j+1), so
+// every fine row is loaded once.  Bitwise the expressions of k_restrict_tau.
+template <typename T, bool NL>
+__global__ void __launch_bounds__(256) k_restrict_tau_seg(const T* __restrict__ u,
+                                                          const T* __restrict__ f,
+                                                          T* __restrict__ uH, T* __restrict__ fH,
+                                                          i64 nf, i64 ld, int B, int mode, i64 seg) {
+  const int r = blockIdx.x * TX + threadIdx.x;
+  if (r >= B) return;
+  const i64 nc = nf / 2;
+  const i64 j0 = ((i64)blockIdx.y * blockDim.y + threadIdx.y) * seg;
+  if (j0 >= nc) return;
+  const i64 j1 = j0 + seg < nc ? j0 + seg : nc;
+  const T ih = inv_h2_of<T>(nf), iH = inv_h2_of<T>(nc);
+  const T* ur = u + r;
+  const T* fr = f + r;
+  T m1 = T(0), Rm = T(0);  // u[2j-1], R u at j-1
+  if (j0 > 0) {
+    T a = __ldg(ur + (2 * j0 - 2) * ld);
+    m1 = __ldg(ur + (2 * j0 - 1) * ld);
+    Rm = xmul(T(0.5), xadd(a, m1));
+  }
+  T c0 = __ldg(ur + (2 * j0) * ld), c1 = __ldg(ur + (2 * j0 + 1) * ld);
+  T Rc = xmul(T(0.5), xadd(c0, c1));
+  constexpr int K = 4;  // coarse rows per batch: all loads of a batch issued first
+  for (i64 jb = j0; jb < j1; jb += K) {
+    T un[2 * K], fv[2 * K];
+#pragma unroll
+    for (int k = 0; k < 2 * K; k++) {
+      i64 iu = 2 * jb + 2 + k, iv = 2 * jb + k;
+      un[k] = __ldg(ur + (iu < nf ? iu : nf - 1) * ld);
+      fv[k] = mode ? __ldg(fr + (iv < nf ? iv : nf - 1) * ld) : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const i64 j = jb + k;
+      if (j >= j1) break;
+      T n0 = T(0), n1 = T(0), Rn = T(0);
+      if (j + 1 < nc) {
+        n0 = un[2 * k];
+        n1 = un[2 * k + 1];
+        Rn = xmul(T(0.5), xadd(n0, n1));
+      }
+      T LH;
+      if (j == 0) LH = xmul(xsub(xmul(T(3), Rc), Rn), iH);
+      else if (j == nc - 1) LH = xmul(xsub(xmul(T(3), Rc), Rm), iH);
+      else LH = xmul(xsub(xsub(xmul(T(2), Rc), Rm), Rn), iH);
+      T L0 = (j == 0) ? xmul(xsub(xmul(T(3), c0), c1), ih)
+                      : xmul(xsub(xsub(xmul(T(2), c0), m1), c1), ih);
+      T L1 = (j == nc - 1) ? xmul(xsub(xmul(T(3), c1), c0), ih)
+                           : xmul(xsub(xsub(xmul(T(2), c1), c0), n0), ih);
+      if (NL) {
+        L0 = xadd(L0, xmul(xmul(c0, c0), c0));
+        L1 = xadd(L1, xmul(xmul(c1, c1), c1));
+        LH = xadd(LH, xmul(xmul(Rc, Rc), Rc));
+      }
+      T tau = xsub(LH, xmul(T(0.5), xadd(L0, L1)));
+      if (mode == 0) {
+        fH[j * ld + r] = tau;
+      } else {
+        T Rf = xmul(T(0.5), xadd(fv[2 * k], fv[2 * k + 1]));
+        fH[j * ld + r] = xadd(Rf, tau);
+        if (mode == 2) uH[j * ld + r] = Rc;
+      }
+      m1 = c1;
+      Rm = Rc;
+      c0 = n0;
+      c1 = n1;
+      Rc = Rn;
+    }
+  }
+}
+
 // cycles.py:120-121: out = u + prolong_correction(uH - restrict(u))
 template <typename T>
 __global__ void k_fas_correct(const T* __restrict__ u, const T* __restrict__ uH, T* __restrict__ out,
@@ -357,7 +431,17 @@ template <typename T>
 void launch_restrict_tau(const T* u, const T* f, T* uH, T* fH, i64 nf, i64 ld, int B, int mode,
                          cudaStream_t s, bool nl) {
   require(nf >= 4 && is_pow2(nf), "tau: fine size must be a power of two >= 4");
-  k_restrict_tau<T><<<grid_for(nf / 2, B), dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode, nl);
+  // segments sized for ~2 resident waves of 256-thread blocks on 148 SMs
+  const i64 nc = nf / 2;
+  const i64 cols = (i64)((B + TX - 1) / TX) * TX;
+  i64 nseg = (148 * 2048) / cols;
+  if (nseg < 1) nseg = 1;
+  i64 seg = (nc + nseg - 1) / nseg;
+  if (seg < 8) seg = 8;
+  nseg = (nc + seg - 1) / seg;
+  dim3 grid((unsigned)((B + TX - 1) / TX), (unsigned)((nseg + TY - 1) / TY));
+  if (nl) k_restrict_tau_seg<T, true><<<grid, dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode, seg);
+  else k_restrict_tau_seg<T, false><<<grid, dim3(TX, TY), 0, s>>>(u, f, uH, fH, nf, ld, B, mode, seg);
   check_launch("restrict_tau");
 }
 
@@ -446,6 +530,7 @@ void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 
   gc.rdiag = (T)(1.0 / (2.0 * inv_h2));
   gc.diag_b = (T)(3.0 * inv_h2);
   gc.omega = (T)omega;
+  gc.diag_i = (T)(2.0 * inv_h2);
   // rdiag must be exact: inv_h2 a power of two (true for every level, 4^k)
   int e;
   require(std::frexp(inv_h2, &e) == 0.5, "gs_sweep: inv_h2 must be a power of two");
@@ -478,6 +563,32 @@ void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* ue
   check_launch("nonlinear_rhs");
 }
 
+// Self-test of the split division of the nonlinear smoother (div_by):
+// q[i] = div_by(x[i], J[i], RN(1/J[i])) and the count of results that differ
+// bitwise from the IEEE division x/J.
+template <typename T>
+__global__ void k_div_check(const T* __restrict__ x, const T* __restrict__ J, T* __restrict__ q,
+                            i64 n, unsigned long long* bad) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const T a = x[i], b = J[i];
+    const T v = div_by(a, b, xrcp(b)), w = xdiv(a, b);
+    if (q) q[i] = v;
+    bool same = sizeof(T) == 8 ? __double_as_longlong((double)v) == __double_as_longlong((double)w)
+                               : __float_as_int((float)v) == __float_as_int((float)w);
+    if (!same && !(v != v && w != w)) atomicAdd(bad, 1ull);
+  }
+}
+
+template <typename T>
+void launch_div_check(const T* x, const T* J, T* q, i64 n, unsigned long long* bad, cudaStream_t s) {
+  require(n >= 0 && x && J && bad, "div_check: bad arguments");
+  if (n == 0) return;
+  i64 blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_div_check<T><<<(unsigned)blocks, 256, 0, s>>>(x, J, q, n, bad);
+  check_launch("div_check");
+}
+
 #define FMGSR_INST(T)                                                                          \
   template void launch_apply_operator<T>(const T*, T*, i64, i64, int, cudaStream_t);          \
   template void launch_restrict<T>(const T*, T*, i64, i64, int, cudaStream_t);                \
@@ -493,7 +604,8 @@ void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* ue
   template void launch_kaczmarz_sweep<T>(T*, const T*, i64, i64, int, i64, i64, double,       \
                                          cudaStream_t);                                        \
   template void launch_fourier_rhs<T>(const double*, int, i64, i64, int, T*, T*, cudaStream_t); \
-  template void launch_nonlinear_rhs<T>(const double*, i64, i64, int, T*, T*, cudaStream_t);
+  template void launch_nonlinear_rhs<T>(const double*, i64, i64, int, T*, T*, cudaStream_t);    \
+  template void launch_div_check<T>(const T*, const T*, T*, i64, unsigned long long*, cudaStream_t);
 FMGSR_INST(double)
 FMGSR_INST(float)
 #undef FMGSR_INST

@@ -155,6 +155,7 @@ static GsCoef<T> make_coef(i64 n, double omega) {
   g.rdiag = (T)(1.0 / (2.0 * inv_h2));  // exact power of two
   g.diag_b = (T)(3.0 * inv_h2);
   g.omega = (T)omega;
+  g.diag_i = (T)(2.0 * inv_h2);
   return g;
 }
 

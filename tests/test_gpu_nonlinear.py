@@ -52,3 +52,56 @@ def test_nonlinear_config3_accuracy(fm):
     err = (torch.linalg.vector_norm(sol - uex, dim=0) / torch.linalg.vector_norm(uex, dim=0))
     h2 = (1.0 / 2 ** m) ** 2
     assert float(err.max()) < 50 * h2  # discretisation error of this problem ~ 8 h^2
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_split_division_is_ieee_division(fm, dtype):
+    """The smoother's x / J (reciprocal of J ahead of the dependency chain +
+    two Markstein corrections) is bitwise the IEEE division: random x over the
+    whole exponent range (incl. zeros, subnormals, inf, nan) against J in the
+    Jacobian's range 2*4^k + 3u^2, plus J at and next to powers of two."""
+    from paper_1207_6720_b200 import _native as N
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n = 1 << 24
+    idt = torch.int64 if dtype == torch.float64 else torch.int32
+    nbits = 64 if dtype == torch.float64 else 32
+    # x: uniformly random bit patterns (every exponent, both signs)
+    raw = torch.randint(-(2 ** (nbits - 1)), 2 ** (nbits - 1) - 1, (n,), generator=g, device="cuda",
+                        dtype=torch.int64).to(idt)
+    x = raw.view(dtype).clone()
+    x[:64] = torch.tensor([0.0, -0.0, float("inf"), float("-inf"), float("nan")] * 12 + [1.0] * 4,
+                          dtype=dtype, device="cuda")
+    k = torch.randint(1, 21, (n,), generator=g, device="cuda").to(dtype)
+    u = torch.randn(n, generator=g, device="cuda", dtype=torch.float64).to(dtype) * \
+        torch.exp2(torch.randint(-30, 12, (n,), generator=g, device="cuda").to(dtype))
+    J = 2 * torch.exp2(2 * k) + 3 * u * u
+    J[: n // 8] = torch.exp2(torch.randint(3, 60, (n // 8,), generator=g, device="cuda").to(dtype))
+    J[n // 8: n // 4] = torch.nextafter(J[: n // 8], torch.tensor(0.0, dtype=dtype, device="cuda"))
+    J[n // 4: 3 * n // 8] = torch.nextafter(J[: n // 8], torch.tensor(float("inf"), dtype=dtype,
+                                                                       device="cuda"))
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    N.call("fmgsr_div_check", dtype, x.data_ptr(), J.data_ptr(), None, n, bad.data_ptr(),
+           N.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+    # moderate magnitudes, where the fast path is taken
+    x2 = torch.randn(n, generator=g, device="cuda", dtype=torch.float64).to(dtype) * 1e3
+    N.call("fmgsr_div_check", dtype, x2.data_ptr(), J.data_ptr(), None, n, bad.data_ptr(),
+           N.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+
+
+@pytest.mark.parametrize("nonlinear", [True, False])
+def test_ns2_omega_matches_oracle(fm, oracle, nonlinear):
+    """V(2,2) streaming smoother with omega != 1 (the OMEGA1 = false kernels)."""
+    B, m = 40, 10
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=2, n_patches=16, buffer=3, omega=0.8,
+                                                     nonlinear=nonlinear))
+    f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=4))
+    oc = oracle.make_cfg(3, m, 1, 2, oracle.GEOM_PATCHES, 16, 3, nonlin=nonlinear, omega=0.8)
+    want = oracle.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=8).T
+    got = fm.fmg_solve(cfg, f)[0].cpu().numpy()
+    assert np.array_equal(got, want)

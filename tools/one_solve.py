@@ -1,0 +1,34 @@
+"""Exactly one plan.solve of a bench workload (for ncu captures with
+--launch-skip: the kernel order of one solve is deterministic).
+
+    python tools/one_solve.py [--workload config2] [--unfused]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1207_6720_b200 as fm  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="config2")
+ap.add_argument("--unfused", action="store_true")
+a = ap.parse_args()
+w = bench.WORKLOADS[a.workload]
+dt = torch.float64 if w["dtype"] == "f64" else torch.float32
+nl = bool(w.get("nonlinear", False))
+cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
+                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
+                                                 nonlinear=nl))
+plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused, use_graph=False))
+if nl:
+    f, _ = fm.nonlinear_batch(2 ** w["m"], fm.nonlinear_scales(w["B"]), dt)
+else:
+    f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+sol = torch.empty_like(f)
+plan.solve(f, sol)
+torch.cuda.synchronize()
+print("ok", a.workload, float(sol.abs().max()))

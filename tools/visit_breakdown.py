@@ -22,10 +22,15 @@ ap.add_argument("--unfused", action="store_true")
 a = ap.parse_args()
 w = bench.WORKLOADS[a.workload]
 dt = torch.float64 if w["dtype"] == "f64" else torch.float32
+nl = bool(w.get("nonlinear", False))
 cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
-                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
+                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
+                                                 nonlinear=nl))
 plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused))
-f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+if nl:
+    f, _ = fm.nonlinear_batch(2 ** w["m"], fm.nonlinear_scales(w["B"]), dt)
+else:
+    f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
 sol = torch.empty_like(f)
 for _ in range(2):
     plan.solve(f, sol)
