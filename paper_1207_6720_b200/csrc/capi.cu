@@ -360,9 +360,10 @@ struct Plan : PlanBase {
   // V(2,2) streaming smoother with the visit prologue fused (kernels_ns2.cu)
   bool ns2_ok(const Level& L) const { return d.fused && d.ns == 2 && L.n >= 8; }
   void smooth_ns2(int l, int src, const T* u_src, const T* uH, bool cr, const T* f, T* out,
-                  cudaStream_t s) {
+                  cudaStream_t s, const Ns2Desc<T>* epi = nullptr) {
     const Level& L = lv[l];
     Ns2Desc<T> c;
+    if (epi) c = *epi;
     c.src = src;
     c.cr = cr;
     c.nonlinear = d.nonlinear != 0;
@@ -468,6 +469,16 @@ struct Plan : PlanBase {
       L.cur ^= 1;
       launch_restrict_tau(L.u[L.cur], ft, uH_out, H.f, L.n, d.ld, (int)d.B, 2, s, d.nonlinear != 0);
       n_launch++;
+    } else if (ns2_ok(L) && L.W >= 4) {  // V(2,2) chain with the restriction fused
+      Ns2Desc<T> e;
+      e.epi = true;
+      e.write_u = !is_sr(t);
+      e.uH_out = uH_out;
+      e.fH_out = H.f;
+      e.E = L.E;
+      e.cnt = L.cnt;
+      smooth_ns2(t, SRC_FMG, nullptr, uH_in, false, ft, L.u[L.cur ^ 1], s, &e);
+      if (e.write_u) L.cur ^= 1;
     } else if (ns2_ok(L)) {
       smooth_ns2(t, SRC_FMG, nullptr, uH_in, false, ft, L.u[L.cur ^ 1], s);
       L.cur ^= 1;
@@ -513,6 +524,17 @@ struct Plan : PlanBase {
       n_launch++;
       if (v.write_u) L.cur ^= 1;
       if (v.uH_out) H.cur ^= 1;
+    } else if (ns2_ok(L) && L.W >= 4) {
+      Ns2Desc<T> e;
+      e.epi = true;
+      e.write_u = !is_sr(l);
+      e.uH_out = (l - 1 == d.m0) ? nullptr : H.u[H.cur ^ 1];
+      e.fH_out = H.f;
+      e.E = L.E;
+      e.cnt = L.cnt;
+      smooth_ns2(l, SRC_LOAD, L.u[L.cur], nullptr, false, L.f, L.u[L.cur ^ 1], s, &e);
+      if (e.write_u) L.cur ^= 1;
+      if (e.uH_out) H.cur ^= 1;
     } else {
       if (ns2_ok(L)) smooth_ns2(l, SRC_LOAD, L.u[L.cur], nullptr, false, L.f, L.u[L.cur ^ 1], s);
       else smooth_into(l, L.u[L.cur], L.f, nullptr, L.u[L.cur ^ 1], s);

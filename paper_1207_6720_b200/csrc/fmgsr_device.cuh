@@ -594,19 +594,34 @@ struct Epilogue {
 
 // Complete coarse cells s/2-1 and s/2 of the patch boundary at fine cell s
 // from the left record (slots 0-4) and the right record (slots 5-9).
+// NL: the records' L values are N u = L u + u^3 (nonlinear tau), and the two
+// fine and two coarse operator values formed here get their cubes added in the
+// k_restrict_tau order.
 template <typename T>
+__device__ __forceinline__ T cube(T x) {
+  return xmul(xmul(x, x), x);
+}
+template <typename T, bool NL = false>
 __device__ __forceinline__ void edge_finish(const T* L, const T* R, T inv_h2, T inv_H2, T& fL,
                                             T& fR) {
   const T um2 = L[0], um1 = L[1], Lm2 = L[2], RuLm1 = L[3], RfL = L[4];
   const T u0 = R[0], u1 = R[1], L1 = R[2], RuRp1 = R[3], RfR = R[4];
   T Lm1 = xmul(xsub(xsub(xmul(T(2), um1), um2), u0), inv_h2);
   T L0 = xmul(xsub(xsub(xmul(T(2), u0), um1), u1), inv_h2);
+  if (NL) {
+    Lm1 = xadd(Lm1, cube(um1));
+    L0 = xadd(L0, cube(u0));
+  }
   T RuL = xmul(T(0.5), xadd(um2, um1));
   T RuR = xmul(T(0.5), xadd(u0, u1));
   T RLL = xmul(T(0.5), xadd(Lm2, Lm1));
   T RLR = xmul(T(0.5), xadd(L0, L1));
   T LHL = xmul(xsub(xsub(xmul(T(2), RuL), RuLm1), RuR), inv_H2);
   T LHR = xmul(xsub(xsub(xmul(T(2), RuR), RuL), RuRp1), inv_H2);
+  if (NL) {
+    LHL = xadd(LHL, cube(RuL));
+    LHR = xadd(LHR, cube(RuR));
+  }
   fL = xadd(RfL, xsub(LHL, RLL));
   fR = xadd(RfR, xsub(LHR, RLR));
 }
@@ -616,7 +631,7 @@ __device__ __forceinline__ void edge_finish(const T* L, const T* R, T inv_h2, T 
 // boundary's counter; the warp that sees an odd old value arrived second and
 // finishes both coarse cells.  Every boundary receives exactly two arrivals
 // per visit, so the parity test stays valid across visits without resets.
-template <typename T>
+template <typename T, bool NL = false>
 __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i64 bi, int side,
                                             const EdgeRec<T>& rec, int lane, int rg, int r,
                                             bool store, T* fH, i64 ld, i64 s, T inv_h2,
@@ -639,7 +654,7 @@ __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i6
       Rr[k] = __ldcg(base + (5 + k) * ldE);
     }
     T fL, fR;
-    edge_finish(Lr, Rr, inv_h2, inv_H2, fL, fR);
+    edge_finish<T, NL>(Lr, Rr, inv_h2, inv_H2, fL, fR);
     if (store) {
       fH[(s / 2 - 1) * ld] = fL;
       fH[(s / 2) * ld] = fR;

@@ -180,6 +180,12 @@ struct Ns2Desc {
   T* u_out = nullptr;
   T* scratch = nullptr;  // (n / W) * (W + 2b + 2) rows of sld
   i64 sld = 0;
+  // fused restriction + tau (T / D visits; nonlinear tau when nonlinear)
+  bool epi = false, write_u = true;
+  T* uH_out = nullptr;
+  T* fH_out = nullptr;
+  T* E = nullptr;
+  int* cnt = nullptr;
 };
 
 template <typename T>
