@@ -282,8 +282,8 @@ def run_gpu(args, w):
     chunks = args.e2e_chunks if B % args.e2e_chunks == 0 else 1
     cplan = fm.get_plan(fm.key_from_config(cfg, B // chunks, dtype))
 
-    def e2e_step():
-        cplan.solve_host(hf, hs, chunks)
+    def e2e_step():  # consecutive batches stream: host inputs are ready at call time
+        cplan.solve_host(hf, hs, chunks, inputs_ready=True)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -348,7 +348,8 @@ def run_gpu(args, w):
             },
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_ms,
-                    "api": "fmgsr_plan_solve_host (pinned host buffers)", "chunks": chunks},
+                    "api": "fmgsr_plan_solve_host_ex (pinned host buffers, FMGSR_HOST_INPUTS_READY: "
+                           "consecutive batches stream)", "chunks": chunks},
             "gpu_launches": info["launches_per_solve"] * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,

@@ -197,6 +197,15 @@ int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stre
  * allocated on the first call. */
 int fmgsr_plan_solve_host(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
                           int64_t chunks, void* stream);
+/* The same with flags.  FMGSR_HOST_INPUTS_READY: h_forcing is ready when the
+ * call is made (filled by the CPU, not by pending work on `stream`), so the
+ * H2D copies are not ordered after prior work on `stream` -- only after the
+ * plan's previous host solve has released its staging buffers.  Consecutive
+ * calls then stream: the H2D of batch k+1 overlaps the D2H of batch k.  The
+ * results are still in h_solution once `stream` reaches the end of the call. */
+#define FMGSR_HOST_INPUTS_READY 1
+int fmgsr_plan_solve_host_ex(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
+                             int64_t chunks, int32_t flags, void* stream);
 /* Same solve launched op by op (no graph) with per-visit CUDA events for
  * profiling: writes up to `cap` visit durations (ms) and their levels. */
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

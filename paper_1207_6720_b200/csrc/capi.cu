@@ -84,7 +84,7 @@ struct PlanBase {
                            int32_t* kind, i64 cap, i64* nv) = 0;
   virtual void info(fmgsr_plan_info* inf) = 0;
   virtual void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
-                          cudaStream_t s) = 0;
+                          cudaStream_t s, int flags) = 0;
 };
 
 template <typename T>
@@ -288,8 +288,9 @@ struct Plan : PlanBase {
   T* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [set][forcing, solution]
   std::vector<cudaEvent_t> hev;  // in_done[2], solved[2], out_done[2]
 
+  bool host_primed = false;  // staging events carry the previous host solve's state
   void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
-                  cudaStream_t s) override {
+                  cudaStream_t s, int flags) override {
     const i64 N = (i64)1 << d.m, B = d.B;
     require(d.ld == B, "solve_host: the plan must be built with ld == B (one chunk)");
     require(chunks >= 1 && ld_host >= chunks * B, "solve_host: ld_host < chunks * B");
@@ -303,11 +304,18 @@ struct Plan : PlanBase {
     }
     cudaEvent_t *in_done = &hev[0], *solved = &hev[2], *out_done = &hev[4];
     const size_t row = (size_t)B * sizeof(T), pitch = (size_t)ld_host * sizeof(T);
-    // the caller's stream orders us after its prior work
-    for (int k = 0; k < 2; k++) {
-      check_cuda(cudaEventRecord(solved[k], s), "ev");
-      check_cuda(cudaEventRecord(out_done[k], s), "ev");
+    // Strict (default): the H2D copies are ordered after prior work on `stream`.
+    // FMGSR_HOST_INPUTS_READY: the host inputs are ready at call time, so the
+    // H2D copies only wait for the staging buffers of the previous host solve
+    // to be released -- consecutive calls stream (this call's H2D overlaps the
+    // previous call's D2H tail).  The solves stay on `stream` either way.
+    if (!(flags & FMGSR_HOST_INPUTS_READY) || !host_primed) {
+      for (int k = 0; k < 2; k++) {
+        check_cuda(cudaEventRecord(solved[k], s), "ev");
+        check_cuda(cudaEventRecord(out_done[k], s), "ev");
+      }
     }
+    host_primed = true;
     for (i64 i = 0; i < chunks; i++) {
       const int k = (int)(i & 1);
       const char* src = (const char*)h_in + i * row;
@@ -1435,10 +1443,15 @@ int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stre
 }
 int fmgsr_plan_solve_host(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
                           int64_t chunks, void* stream) {
+  return fmgsr_plan_solve_host_ex(plan, h_forcing, h_solution, ld_host, chunks, 0, stream);
+}
+int fmgsr_plan_solve_host_ex(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
+                             int64_t chunks, int32_t flags, void* stream) {
   return guarded([&] {
     require(plan && h_forcing && h_solution, "plan_solve_host: null argument");
+    require((flags & ~FMGSR_HOST_INPUTS_READY) == 0, "plan_solve_host: unknown flags");
     reinterpret_cast<PlanBase*>(plan)->solve_host(h_forcing, h_solution, ld_host, chunks,
-                                                  S(stream));
+                                                  S(stream), flags);
   });
 }
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

@@ -101,19 +101,23 @@ class FmgPlan:
                                          N.stream_ptr()), "plan_solve")
         return out
 
-    def solve_host(self, forcing: torch.Tensor, out: torch.Tensor, chunks: int) -> torch.Tensor:
+    def solve_host(self, forcing: torch.Tensor, out: torch.Tensor, chunks: int,
+                   inputs_ready: bool = False) -> torch.Tensor:
         """End-to-end solve from HOST memory: ``forcing`` / ``out`` are pinned CPU
         tensors of shape (2**m, chunks * B); chunks of B right-hand sides are
         pipelined H2D / solve / D2H on separate streams.  Returns ``out`` once
-        the current stream has reached the end of the pipeline."""
+        the current stream has reached the end of the pipeline.  With
+        ``inputs_ready`` the host forcing is taken as ready at call time, so
+        consecutive calls stream (FMGSR_HOST_INPUTS_READY)."""
         k = self.key
         for name, t in (("forcing", forcing), ("solution", out)):
             if t.is_cuda or t.dtype != k.dtype or tuple(t.shape) != (self.N, chunks * k.B) \
                     or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous host {k.dtype} tensor of shape "
                                  f"({self.N}, {chunks * k.B})")
-        N.check(N.lib().fmgsr_plan_solve_host(self._h, forcing.data_ptr(), out.data_ptr(),
-                                              chunks * k.B, chunks, N.stream_ptr()),
+        N.check(N.lib().fmgsr_plan_solve_host_ex(self._h, forcing.data_ptr(), out.data_ptr(),
+                                                 chunks * k.B, chunks, int(bool(inputs_ready)),
+                                                 N.stream_ptr()),
                 "plan_solve_host")
         return out
 

@@ -215,3 +215,21 @@ def test_solve_host_pipelined_matches_device_solve(fm):
     plan.solve_host(hf, hs, chunks)
     torch.cuda.current_stream().synchronize()
     assert torch.equal(hs, want)
+
+
+def test_solve_host_streaming_consecutive_batches(fm):
+    """FMGSR_HOST_INPUTS_READY: back-to-back host solves of different batches
+    overlap on the copy streams and each lands its own exact solution."""
+    m, B, chunks = 11, 64, 4
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=64, buffer=4))
+    plan = fm.get_plan(fm.key_from_config(cfg, B // chunks, torch.float64))
+    fs = [fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=30 + i))[0] for i in range(3)]
+    wants = [fm.fmg_solve(cfg, f)[0].cpu() for f in fs]
+    hfs = [f.cpu().pin_memory() for f in fs]
+    hss = [torch.zeros_like(h).pin_memory() for h in hfs]
+    for hf, hs in zip(hfs, hss):
+        plan.solve_host(hf, hs, chunks, inputs_ready=True)
+    torch.cuda.current_stream().synchronize()
+    for hs, want in zip(hss, wants):
+        assert torch.equal(hs, want)
