@@ -114,7 +114,7 @@ struct Plan : PlanBase {
   std::vector<int32_t> ev_lvl, ev_kind;
   bool timing = false;
   // coarse hierarchy kernel: levels m0..Lc on chip, CW RHS columns per CTA
-  bool use_coarse = false;
+  bool use_coarse = false, coarse_warp = true;
   int Lc = 0, CW = 1;
   int coarse_trace = 0;
   // patch-slab sharding: levels > Lr are split into S slabs, this is slab srank;
@@ -163,10 +163,46 @@ struct Plan : PlanBase {
     }
     // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
     // three fields per level (two u, f) for CW columns fit in ~200 KB.
-    use_coarse = d.fused && d.ns == 1 && d.coarse != 0 && !d.nonlinear;
+    // Two coarse kernels: one warp per RHS column (default; ns 1 or 2, linear or
+    // nonlinear) or one CTA per CW columns (FMGSR_COARSE=cta; ns = 1 linear).
+    // The CTA kernel is faster where it applies (measured: config 2 3.30 vs
+    // 3.70 ms); the warp kernel carries ns = 2 and the nonlinear smoother.
+    const char* ck = getenv("FMGSR_COARSE");
+    coarse_warp = (d.ns != 1 || d.nonlinear) || (ck && std::string(ck) == "warp");
+    use_coarse = d.fused && d.coarse != 0 && (d.ns == 1 || d.ns == 2) && d.m - d.m0 >= 2;
     const char* tr = getenv("FMGSR_COARSE_TRACE");
     coarse_trace = (tr && tr[0] == '1') ? 1 : 0;
-    if (use_coarse) {
+    if (use_coarse && coarse_warp) {
+      // deepest Lc whose per-warp slice fits and keeps all B warps in one wave
+      CW = 1;
+      Lc = m0;
+      int dev = 0, smsm = 0, nsm = 0;
+      check_cuda(cudaGetDevice(&dev), "device");
+      check_cuda(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem/SM");
+      check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
+      auto fits = [&](int lc) {
+        CoarseArgs<T> t;
+        t.m0 = m0;
+        t.Lc = lc;
+        for (int l = m0; l <= lc; l++) {
+          t.W[l] = lv[l].W;
+          t.b[l] = lv[l].b;
+        }
+        const size_t bytes = coarse_warp_layout(t, d.ns == 2, d.nonlinear != 0);
+        if (bytes > 227 * 1024) return false;
+        // one chain per lane: a warp's serial work grows with P_l / 32
+        // (config 3: Lc = 6 measured best against 8..11)
+        if (lv[lc].n / lv[lc].W > 32) return false;
+        i64 per_sm = (i64)smsm / (i64)(bytes + 1024);
+        if (per_sm > 32) per_sm = 32;
+        return per_sm >= 1 && per_sm * nsm >= d.B;
+      };
+      while (Lc + 1 <= m - 1 && fits(Lc + 1)) Lc++;
+      int want = d.coarse;
+      if (want < 0)
+        if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
+      if (want > 0 && want - 1 >= m0 && want - 1 < Lc) Lc = want - 1;
+    } else if (use_coarse) {
       i64 cw = 1;
       // ~128 CTAs (one wave on 148 SMs); measured best against 256 / 512
       i64 target = 128;
@@ -629,6 +665,10 @@ struct Plan : PlanBase {
     }
   }
 
+  void launch_coarse_any(const CoarseArgs<T>& a, cudaStream_t s) {
+    if (coarse_warp) launch_coarse_warp(a, d.ns == 2, d.nonlinear != 0, s);
+    else launch_coarse(a, s);
+  }
   CoarseArgs<T> coarse_args(int mode) const {
     CoarseArgs<T> a;
     a.m0 = d.m0;
@@ -722,7 +762,7 @@ struct Plan : PlanBase {
         mark_begin(s, Lc, VK_COARSE);
         CoarseArgs<T> a = coarse_args(0);
         a.u_top = lv[Lc].u[lv[Lc].cur];
-        launch_coarse(a, s);
+        launch_coarse_any(a, s);
         n_launch++;
         mark_end(s);
         break;
@@ -738,7 +778,7 @@ struct Plan : PlanBase {
         CoarseArgs<T> a = coarse_args(1);
         a.u_top = lv[Lc].u[lv[Lc].cur];  // restricted u_{Lc} in, V-cycled u_{Lc} out (in place)
         a.f_top = lv[Lc].f;
-        launch_coarse(a, s);
+        launch_coarse_any(a, s);
         n_launch++;
         mark_end(s);
         break;

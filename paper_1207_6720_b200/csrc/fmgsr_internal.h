@@ -78,9 +78,15 @@ struct CoarseArgs {
   double omega = 1.0;
   KzCoef<T> kz{};
   int trace = 0;  // debug: per-phase clock printf from CTA 0
+  // warp-per-column kernel layout (filled by coarse_warp_layout)
+  int lgW[32] = {}, off[32] = {}, slen[32] = {};
+  int fields = 0, scratch = 0;
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
 template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW);
+// one warp per RHS column (kernels_coarse_warp.cu): ns = 1 or 2, linear or nonlinear
+template <typename T> size_t coarse_warp_layout(CoarseArgs<T>& a, bool ns2, bool nl);
+template <typename T> void launch_coarse_warp(const CoarseArgs<T>& a, bool ns2, bool nl, cudaStream_t s);
 
 // Multi-level restriction (f cascade): p[k] receives level (src_level-1-k)
 template <typename T>

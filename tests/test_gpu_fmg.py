@@ -233,3 +233,19 @@ def test_solve_host_streaming_consecutive_batches(fm):
     torch.cuda.current_stream().synchronize()
     for hs, want in zip(hss, wants):
         assert torch.equal(hs, want)
+
+
+@pytest.mark.parametrize("m,P,b,n_sr", [(12, 64, 4, 1), (11, 16, 1, 2), (12, 4096, 8, 1)])
+def test_warp_coarse_kernel_matches_oracle(fm, oracle, monkeypatch, m, P, b, n_sr):
+    """The warp-per-column coarse kernel (default for V(2,2) / nonlinear,
+    FMGSR_COARSE=warp for V(1,1)) on the linear V(1,1) path, bit for bit."""
+    monkeypatch.setenv("FMGSR_COARSE", "warp")
+    B = 33  # a batch no other test uses: fresh plans read the environment
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=P, buffer=b))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + b))
+    want = oracle.fmg_solve_batch(oracle_cfg(oracle, cfg), np.ascontiguousarray(f.cpu().numpy().T),
+                                  nthreads=8).T
+    for kw in (dict(), dict(coarse=m - 2), dict(coarse=5)):
+        got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
+        assert np.array_equal(got, want), kw
