@@ -1,7 +1,8 @@
-"""Run a few FMG solves op by op (no CUDA graph) for ncu: every level visit is
-its own launch in a deterministic order.
+"""Run a few FMG solves of a bench workload op by op (no CUDA graph) for ncu:
+every level visit is its own launch in a deterministic order, so
+``ncu -k regex:<kernel> --launch-skip K -c 1`` picks one visit.
 
-    python tools/profile_solve.py [--workload config2] [--solves 1] [--graph]
+    python tools/profile_solve.py [--workload config2] [--solves 1] [--graph] [--unfused]
 """
 import argparse
 import os
@@ -17,15 +18,21 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="config2")
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--unfused", action="store_true")
 a = ap.parse_args()
 w = bench.WORKLOADS[a.workload]
 dt = torch.float64 if w["dtype"] == "f64" else torch.float32
+nl = bool(w.get("nonlinear", False))
 cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
-                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"]))
-plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, use_graph=a.graph))
-f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+                      smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
+                                                 nonlinear=nl))
+plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused, use_graph=a.graph))
+if nl:
+    f, _ = fm.nonlinear_batch(2 ** w["m"], fm.nonlinear_scales(w["B"]), dt)
+else:
+    f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
 sol = torch.empty_like(f)
 for _ in range(a.solves):
     plan.solve(f, sol)
 torch.cuda.synchronize()
-print("solves done", a.solves, plan.info())
+print("solves done", a.workload, a.solves, plan.info())
