@@ -144,6 +144,11 @@ int fmgsr_fourier_rhs_f32(const double* coef, int K, int64_t n, int64_t B, int64
 int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* stream);
 int fmgsr_nonlinear_rhs_f32(const double* scale, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* stream);
 
+/* the study harness's manufactured problem (reference problem.py:23-46) for
+ * one RHS on the device: f[i] = sum over odd j <= nmodes of sin(j pi x_i)/j,
+ * uex[i] = sum sin(j pi x_i)/(j (j pi)^2), x_i = (i + 1/2)/n; uex may be NULL */
+int fmgsr_manufactured_rhs_f64(int64_t n, int64_t nmodes, double* f, double* uex, void* stream);
+
 /* ---- Self-test (not on the solve path) ----------------------------------
  * The nonlinear smoother divides x / J with a reciprocal of J computed ahead
  * of the Gauss-Seidel dependency chain plus two Markstein corrections.  This

@@ -70,6 +70,7 @@ _SIGS = {
     "fmgsr_nonlinear_rhs": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_smooth_scratch_rows": (_i64, [_i64, _i64, _i64]),
     "fmgsr_div_check": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "fmgsr_manufactured_rhs_f64": (C.c_int, [_i64, _i64, _vp, _vp, _vp]),
     "fmgsr_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_vp)]),
     "fmgsr_plan_destroy": (C.c_int, [_vp]),
     "fmgsr_plan_get_info": (C.c_int, [_vp, C.POINTER(PlanInfo)]),

@@ -1382,6 +1382,9 @@ int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t l
 int fmgsr_nonlinear_rhs_f32(const double* scale, int64_t n, int64_t B, int64_t ld, float* f, float* uex, void* s) {
   return guarded([&] { check_field(n, B, ld, "nonlinear_rhs"); launch_nonlinear_rhs<float>(scale, n, ld, (int)B, f, uex, S(s)); });
 }
+int fmgsr_manufactured_rhs_f64(int64_t n, int64_t nmodes, double* f, double* uex, void* s) {
+  return guarded([&] { launch_manufactured(n, nmodes, f, uex, S(s)); });
+}
 int fmgsr_div_check_f64(const double* x, const double* J, double* q, int64_t n, unsigned long long* bad, void* s) {
   return guarded([&] { launch_div_check<double>(x, J, q, n, bad, S(s)); });
 }

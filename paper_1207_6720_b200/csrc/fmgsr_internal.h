@@ -213,6 +213,7 @@ template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, 
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);
 template <typename T> void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop, double proj_diag, cudaStream_t s);
 template <typename T> void launch_fourier_rhs(const double* coef, int K, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
+void launch_manufactured(i64 n, i64 K, double* f, double* uex, cudaStream_t s);
 template <typename T> void launch_div_check(const T* x, const T* J, T* q, i64 n, unsigned long long* bad, cudaStream_t s);
 template <typename T> void launch_nonlinear_rhs(const double* scale, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);
 

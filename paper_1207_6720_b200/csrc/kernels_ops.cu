@@ -384,6 +384,24 @@ __global__ void k_fourier_rhs(const double* __restrict__ coef, int K, i64 n, i64
   }
 }
 
+// The study harness's manufactured problem (reference problem.py:23-46):
+// f = sum over odd j <= K of sin(j pi x)/j, u = sum sin(j pi x)/(j (j pi)^2),
+// one thread per cell (a single right-hand side, ld = 1).
+__global__ void k_manufactured(i64 n, i64 K, double* f, double* uex) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const double x = ((double)i + 0.5) / (double)n;
+    double fs = 0.0, us = 0.0;
+    for (i64 j = 1; j <= K; j += 2) {
+      const double s = sinpi((double)j * x);
+      const double jp = (double)j * M_PI;
+      fs += s / (double)j;
+      us += s / ((double)j * (jp * jp));
+    }
+    f[i] = fs;
+    if (uex) uex[i] = us;
+  }
+}
+
 // Nonlinear manufactured problem (BASELINE config 3): u = s x(1-x)e^x,
 // f = s x(x+3)e^x + (s x(1-x)e^x)^3 for -u'' + u^3 = f.
 template <typename T>
@@ -402,6 +420,15 @@ __global__ void k_nonlinear_rhs(const double* __restrict__ scale, i64 n, i64 ld,
 }
 
 }  // namespace
+
+void launch_manufactured(i64 n, i64 K, double* f, double* uex, cudaStream_t s) {
+  require(n >= 1 && K >= 1 && f, "manufactured_rhs: bad arguments");
+  i64 blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_manufactured<<<(unsigned)blocks, 256, 0, s>>>(n, K, f, uex);
+  check_launch("manufactured_rhs");
+}
+
 
 template <typename T>
 void launch_apply_operator(const T* u, T* out, i64 n, i64 ld, int B, cudaStream_t s) {

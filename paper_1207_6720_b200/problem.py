@@ -60,6 +60,15 @@ def rel_l2_error(u, u_ref) -> float:
     """Plain relative 2-norm error (problem.py:49-58); max over RHS for a batch."""
     if F.length(u) != F.length(u_ref):
         raise ValueError(f"field sizes differ: {F.length(u)} vs {F.length(u_ref)}")
+    if not isinstance(u, torch.Tensor) and not isinstance(u_ref, torch.Tensor) \
+            and np.ndim(u) == 1 and np.ndim(u_ref) == 1:
+        # host vectors: numpy's norm, the reference's exact reduction
+        a1 = np.asarray(u, dtype=np.float64)
+        b1 = np.asarray(u_ref, dtype=np.float64)
+        den1 = float(np.linalg.norm(b1))
+        if den1 == 0.0:
+            raise ValueError("reference field has zero norm")
+        return float(np.linalg.norm(a1 - b1)) / den1
     a = torch.as_tensor(np.asarray(u) if not isinstance(u, torch.Tensor) else u,
                         dtype=torch.float64)
     b = torch.as_tensor(np.asarray(u_ref) if not isinstance(u_ref, torch.Tensor) else u_ref,
