@@ -211,6 +211,15 @@ int fmgsr_plan_solve_host(void* plan, const void* h_forcing, void* h_solution, i
 #define FMGSR_HOST_INPUTS_READY 1
 int fmgsr_plan_solve_host_ex(void* plan, const void* h_forcing, void* h_solution, int64_t ld_host,
                              int64_t chunks, int32_t flags, void* stream);
+/* Functional-only output (the paper's "compute a functional of
+ * u"): the same FMG cycle, but the final up visit reduces, per right-hand
+ * side r, J_r = sum_i w[i][r] u[i][r] (weights: DEVICE [2^m][ld], or NULL for
+ * the midpoint-rule integral h * sum_i u[i][r]) instead of writing u_m -- the
+ * finest level is never stored.  functional: DEVICE array of B values (the
+ * plan's dtype).  Summation order: per patch over its owned cells, then over
+ * patches in order, so the result is deterministic. */
+int fmgsr_plan_solve_functional(void* plan, const void* forcing, const void* weights,
+                                void* functional, void* stream);
 /* Same solve launched op by op (no graph) with per-visit CUDA events for
  * profiling: writes up to `cap` visit durations (ms) and their levels. */
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

@@ -77,6 +77,7 @@ _SIGS = {
     "fmgsr_plan_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fmgsr_plan_solve_host": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "fmgsr_plan_solve_host_ex": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
+    "fmgsr_plan_solve_functional": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "fmgsr_plan_solve_timed": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                                          C.POINTER(_i64)]),
     "fmgsr_nccl_unique_id": (C.c_int, [_vp]),

@@ -12,8 +12,10 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
 #include <map>
 #include <memory>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -85,6 +87,7 @@ struct PlanBase {
   virtual void info(fmgsr_plan_info* inf) = 0;
   virtual void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
                           cudaStream_t s, int flags) = 0;
+  virtual void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) = 0;
 };
 
 template <typename T>
@@ -591,14 +594,65 @@ struct Plan : PlanBase {
     mark_end(s);
   }
 
+  // functional output mode (solve_functional): the final up visit reduces
+  // J = scale * sum_i w_i u_i instead of writing u_m
+  bool fun_mode = false;
+  const T* fun_w = nullptr;
+  T* fun_out = nullptr;
+  T* fun_part = nullptr;  // [P_m][Bp] partial sums
+  std::map<std::tuple<const void*, const void*, void*>, cudaGraphExec_t> fgraphs;
+
+  void final_functional(int l, const T* fl, const T* uH, bool sr, cudaStream_t s) {
+    Level& L = lv[l];
+    const i64 P = L.n / L.W;
+    const T scale = fun_w ? T(1) : (T)std::ldexp(1.0, -l);  // unit weights: h * sum u
+    if (fused_chain_ok()) {  // the reduction rides in the visit: u_m is never stored
+      VisitDesc<T> v;
+      v.src = sr ? SRC_FMG : SRC_CORR;
+      v.cr = sr;
+      v.n = L.n;
+      v.ld = d.ld;
+      v.B = (int)d.B;
+      v.W = L.W;
+      v.b = L.b;
+      v.omega = d.omega;
+      v.u_src = sr ? nullptr : L.u[L.cur];
+      v.uH = uH;
+      v.f = fl;
+      v.u_out = nullptr;
+      v.fun_w = fun_w;
+      v.fun_part = fun_part;
+      launch_visit(v, s);
+    } else {  // other smoothers: the field, then the same ordered reduction
+      T* u = L.u[L.cur ^ 1];
+      if (ns2_ok(L)) {
+        smooth_ns2(l, sr ? SRC_FMG : SRC_CORR, sr ? nullptr : L.u[L.cur], uH, sr, fl, u, s);
+      } else {
+        Level& H = lv[l - 1];
+        if (sr) launch_prolong_fmg(uH, tmp, H.n, d.ld, (int)d.B, s);
+        else launch_fas_correct(L.u[L.cur], uH, tmp, L.n, d.ld, (int)d.B, s);
+        n_launch++;
+        smooth_into(l, tmp, fl, sr ? uH : nullptr, u, s);
+      }
+      launch_functional_field(u, fun_w, L.n, L.W, d.ld, (int)d.B, fun_part, s);
+    }
+    n_launch += 2;
+    launch_functional_reduce(fun_part, P, (int)d.B, scale, fun_out, s);
+  }
+
   // Up leg at level l: correction (non-SR) or full update + CR (SR), smooth.
-  void visit_up(int l, const T* fl, T* dst, cudaStream_t s) {
+  void visit_up(int l, const T* fl, T* dst, cudaStream_t s, bool final = false) {
     Level& L = lv[l];
     Level& H = lv[l - 1];
     mark_begin(s, l, VK_UP);
     T* out = dst ? dst : L.u[L.cur ^ 1];
     const T* uH = H.u[H.cur];
     const bool sr = is_sr(l);
+    if (final && fun_mode) {
+      final_functional(l, fl, uH, sr, s);
+      mark_end(s);
+      return;
+    }
     if (fused_chain_ok()) {
       VisitDesc<T> v;
       v.src = sr ? SRC_FMG : SRC_CORR;
@@ -660,7 +714,7 @@ struct Plan : PlanBase {
       visit_direct(s);                                     // smooth_level at m0
       for (int l = m0 + 1; l <= t; l++) {                  // cycles.py:118-133
         const T* fl = (l == m) ? forcing : lv[l].f;
-        visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s);
+        visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s, l == m && t == m);
       }
     }
   }
@@ -786,7 +840,7 @@ struct Plan : PlanBase {
       case ST_UP: {
         const bool fin = st.l == d.m && st.t == d.m;
         T* dst = fin ? (S > 1 ? solution - c0(d.m) * d.ld : solution) : nullptr;
-        visit_up(st.l, flev(st.l, forcing), dst, s);
+        visit_up(st.l, flev(st.l, forcing), dst, s, fin);
         break;
       }
     }
@@ -917,6 +971,47 @@ struct Plan : PlanBase {
         graphs.erase(graphs.begin());
       }
       it = graphs.emplace(key, ex).first;
+    }
+    check_cuda(cudaGraphLaunch(it->second, s), "graph launch");
+  }
+
+  void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) override {
+    require(S == 1, "solve_functional: not available on sharded plans");
+    if (!fun_part) {  // before any capture: [P_m][Bp] partial sums
+      const Level& L = lv[d.m];
+      fun_part = alloc((size_t)(L.n / L.W) * (((d.B + 31) / 32) * 32) * sizeof(T));
+    }
+    auto key = std::make_tuple(in, w, out);
+    auto it = fgraphs.find(key);
+    fun_w = (const T*)w;
+    fun_out = (T*)out;
+    fun_mode = true;
+    struct Reset {
+      bool& m;
+      ~Reset() { m = false; }
+    } reset{fun_mode};
+    if (!d.use_graph) {
+      enqueue((const T*)in, nullptr, s);
+      return;
+    }
+    if (it == fgraphs.end()) {
+      cudaGraph_t g;
+      check_cuda(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue((const T*)in, nullptr, cap);
+      } catch (...) {
+        cudaStreamEndCapture(cap, &g);
+        throw;
+      }
+      check_cuda(cudaStreamEndCapture(cap, &g), "end capture");
+      cudaGraphExec_t ex;
+      check_cuda(cudaGraphInstantiate(&ex, g, 0), "graph instantiate");
+      cudaGraphDestroy(g);
+      if (fgraphs.size() >= 8) {
+        cudaGraphExecDestroy(fgraphs.begin()->second);
+        fgraphs.erase(fgraphs.begin());
+      }
+      it = fgraphs.emplace(key, ex).first;
     }
     check_cuda(cudaGraphLaunch(it->second, s), "graph launch");
   }
@@ -1495,6 +1590,13 @@ int fmgsr_plan_solve_host_ex(void* plan, const void* h_forcing, void* h_solution
     require((flags & ~FMGSR_HOST_INPUTS_READY) == 0, "plan_solve_host: unknown flags");
     reinterpret_cast<PlanBase*>(plan)->solve_host(h_forcing, h_solution, ld_host, chunks,
                                                   S(stream), flags);
+  });
+}
+int fmgsr_plan_solve_functional(void* plan, const void* forcing, const void* weights,
+                                void* functional, void* stream) {
+  return guarded([&] {
+    require(plan && forcing && functional, "plan_solve_functional: null argument");
+    reinterpret_cast<PlanBase*>(plan)->solve_functional(forcing, weights, functional, S(stream));
   });
 }
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

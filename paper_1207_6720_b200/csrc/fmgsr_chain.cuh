@@ -24,13 +24,18 @@
 
 namespace fmgsr {
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D, bool BULK>
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D, bool BULK,
+          bool FUNC = false>
 struct Chain {
   static constexpr int R = SrcRows<SRC, CR>::R;
   PairSource<T, SRC, CR> src;
   GsCoef<T> gc;
   i64 n, nc, ld, ws, os, oe;
   T* out;  // u_l output, column-offset (nullptr: not written)
+  // FUNC: instead of writing the owned cells, accumulate sum_i w_i u_i over
+  // them in cell order (w column-offset; nullptr: unit weights)
+  const T* fw;
+  T facc;
   bool store;
   T* ring;  // this lane's ring: slot s, row k at ring[(s * R + k) * NT]
   Epilogue<T>* epi;
@@ -108,6 +113,9 @@ struct Chain {
         }
         epi->push(q, n0, n1, f0, f1, store);
       }
+    } else if (FUNC) {
+      if (i0 >= os && i0 < oe) facc = xadd(facc, fw ? xmul(fw[i0 * ld], n0) : n0);
+      if (i1 >= os && i1 < oe) facc = xadd(facc, fw ? xmul(fw[i1 * ld], n1) : n1);
     } else if (store) {
       if (i0 >= os && i0 < oe) out[i0 * ld] = n0;
       if (i1 >= os && i1 < oe) out[i1 * ld] = n1;
@@ -125,6 +133,7 @@ struct Chain {
     T* po = (OWNED && out) ? out + (2 * q) * ld : nullptr;
     if (EPI && OWNED) epi->fast_begin(q);
     const bool st_u = OWNED && out && store;
+    const T* pw = (FUNC && OWNED && fw) ? fw + (2 * q) * ld : nullptr;
 #pragma unroll 2
     for (; q <= q_end; q++) {
       await(q + 1);
@@ -141,7 +150,16 @@ struct Chain {
       T n1 = gsi(n0, v1, w0, f1);
       uL = n1;
       if (OWNED) {
-        if (st_u) {
+        if (FUNC) {
+          if (pw) {
+            facc = xadd(facc, xmul(pw[0], n0));
+            facc = xadd(facc, xmul(pw[ld], n1));
+            pw += 2 * ld;
+          } else {
+            facc = xadd(facc, n0);
+            facc = xadd(facc, n1);
+          }
+        } else if (st_u) {
           po[0] = n0;
           po[ld] = n1;
         }

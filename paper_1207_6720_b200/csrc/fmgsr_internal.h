@@ -132,7 +132,17 @@ struct VisitDesc {
   i64 qlo = -1, qhi = -1;
   T* E_out = nullptr;
   bool left_remote = false, right_remote = false;
+  // functional output (final up visit): partial sums instead of the field
+  const T* fun_w = nullptr;
+  T* fun_part = nullptr;  // [P][round_up(B, 32)]
 };
+
+// functional J = scale * sum_p sum_{owned i} w_i u_i (w nullptr: unit weights)
+template <typename T>
+void launch_functional_field(const T* u, const T* w, i64 n, i64 W, i64 ld, int B, T* part,
+                             cudaStream_t s);
+template <typename T>
+void launch_functional_reduce(const T* part, i64 P, int B, T scale, T* out, cudaStream_t s);
 
 // Complete the owned coarse cell at a shard's slab boundary from the two edge
 // records (own outbox slot, neighbour's record received in the inbox).

@@ -33,6 +33,8 @@ struct VisitArgs {
   T *u_out, *uH_out, *fH_out, *E;
   int* cnt;
   const i64 *olo, *ohi, *elo, *ehi;
+  const T* fun_w;  // FUNC: weights (nullptr: unit)
+  T* fun_part;     // FUNC: per-(patch, column) partial sums [P][nrg * 32]
 };
 
 constexpr int VNT = 128;  // threads per block of the visit kernel
@@ -47,7 +49,7 @@ __host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one
   return visit_ring_bytes<T, SRC, CR>() + (size_t)(VNT / 32) * VD * 8;
 }
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK>
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC>
 __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
     we = oe + a.b < a.n ? oe + a.b : a.n;
   }
 
-  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD, BULK> ch;
+  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD, BULK, FUNC> ch;
   ch.lane = lane;
   ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR>()) +
             (threadIdx.x >> 5) * VD;
@@ -104,9 +106,12 @@ __global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
   ch.store = store;
   ch.ring = reinterpret_cast<T*>(visit_smem) + threadIdx.x;
   ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + r : nullptr;
+  ch.fw = (FUNC && a.fun_w) ? a.fun_w + rr : nullptr;
+  ch.facc = T(0);
   if (!EPI) {
     ch.epi = nullptr;
     ch.run(we);
+    if (FUNC) a.fun_part[p * ((i64)a.nrg * 32) + r] = ch.facc;
     return;
   }
   Epilogue<T> ep;
@@ -179,10 +184,10 @@ static KzCoef<T> make_kz(double pd) {
   return k;
 }
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK>
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC = false>
 static void launch_visit_k(const VisitArgs<T>& a, i64 blocks, cudaStream_t s) {
   constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
-  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK>;
+  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC>;
   static bool attr = false;
   if (!attr && smem > 48 * 1024) {
     check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -210,6 +215,19 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   // queue: sources with >= 5 staged rows per pair (the FAS-correction visits);
   // measured slower than cp.async for 3-4 rows (profiles/r01 notes)
   const bool bulk = SrcRows<SRC, CR>::R >= 5 && bulk_ok(a);
+  // functional output of the final up visit (non-SR: FAS correction; SR: Pi + CR)
+  if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
+    if (a.fun_part) {
+      if (om1) {
+        if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true, true>(a, blocks, s);
+        else launch_visit_k<T, SRC, CR, EPI, true, false, true>(a, blocks, s);
+      } else {
+        if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true, true>(a, blocks, s);
+        else launch_visit_k<T, SRC, CR, EPI, false, false, true>(a, blocks, s);
+      }
+      return;
+    }
+  }
   if (om1) {
     if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true>(a, blocks, s);
     else launch_visit_k<T, SRC, CR, EPI, true, false>(a, blocks, s);
@@ -253,6 +271,11 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   a.E_out = d.E_out;
   a.left_remote = d.left_remote;
   a.right_remote = d.right_remote;
+  a.fun_w = d.fun_w;
+  a.fun_part = d.fun_part;
+  require(!d.fun_part || (!d.epi && !d.olo && d.p_count < 0 &&
+                          ((d.src == SRC_FMG && d.cr) || (d.src == SRC_CORR && !d.cr))),
+          "visit: functional output only on a final up visit");
   if (d.olo) {
     require(d.src == SRC_LOAD && !d.epi, "visit: patch arrays only with plain loads");
     a.P = d.P;
@@ -279,7 +302,7 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
     require(d.W >= 4 && d.n >= 8, "visit: fused restriction needs owned width >= 4");
     require(d.fH_out && d.E && d.cnt, "visit: epilogue buffers missing");
   } else {
-    require(d.u_out != nullptr, "visit: u_out is null");
+    require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
   if (a.P == 0) return;
 #define FMGSR_DISPATCH(SRCV)                                                    \
@@ -461,6 +484,50 @@ __global__ void k_edge_fix(const T* __restrict__ L, const T* __restrict__ R, T* 
   if (which != 1) fH[(s / 2 - 1) * ld + r] = fL;  // 0: left cell, 1: right cell, 2: both
   if (which != 0) fH[(s / 2) * ld + r] = fR;
 }
+
+// Functional of a stored field with the fused visit's summation order: per
+// (patch, column) a sequential sum of w_i u_i over the owned cells, then
+// (k_functional_reduce) a sequential sum over patches, times `scale`.
+template <typename T>
+__global__ void k_functional_field(const T* __restrict__ u, const T* __restrict__ w, i64 n, i64 W,
+                                   i64 ld, int B, T* part, i64 ldp) {
+  const i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const i64 P = n / W;
+  if (k >= P * ldp) return;
+  const i64 p = k / ldp;
+  const int r = (int)(k - p * ldp);
+  const int rr = r < B ? r : B - 1;
+  T acc = T(0);
+  for (i64 i = p * W; i < (p + 1) * W; i++)
+    acc = xadd(acc, w ? xmul(w[i * ld + rr], u[i * ld + rr]) : u[i * ld + rr]);
+  part[p * ldp + r] = acc;
+}
+template <typename T>
+__global__ void k_functional_reduce(const T* __restrict__ part, i64 P, i64 ldp, int B, T scale,
+                                    T* out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  T acc = T(0);
+  for (i64 p = 0; p < P; p++) acc = xadd(acc, part[p * ldp + r]);
+  out[r] = xmul(acc, scale);
+}
+template <typename T>
+void launch_functional_field(const T* u, const T* w, i64 n, i64 W, i64 ld, int B, T* part,
+                             cudaStream_t s) {
+  const i64 ldp = ((B + 31) / 32) * 32, items = (n / W) * ldp;
+  k_functional_field<T><<<(unsigned)((items + 255) / 256), 256, 0, s>>>(u, w, n, W, ld, B, part, ldp);
+  check_launch("functional_field");
+}
+template <typename T>
+void launch_functional_reduce(const T* part, i64 P, int B, T scale, T* out, cudaStream_t s) {
+  const i64 ldp = ((B + 31) / 32) * 32;
+  k_functional_reduce<T><<<(B + 127) / 128, 128, 0, s>>>(part, P, ldp, B, scale, out);
+  check_launch("functional_reduce");
+}
+template void launch_functional_field<double>(const double*, const double*, i64, i64, i64, int, double*, cudaStream_t);
+template void launch_functional_field<float>(const float*, const float*, i64, i64, i64, int, float*, cudaStream_t);
+template void launch_functional_reduce<double>(const double*, i64, int, double, double*, cudaStream_t);
+template void launch_functional_reduce<float>(const float*, i64, int, float, float*, cudaStream_t);
 
 template <typename T>
 void launch_edge_fix(const T* rec_left, const T* rec_right, T* fH, i64 s, i64 nf, i64 ld, int B,

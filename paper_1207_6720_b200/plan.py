@@ -101,6 +101,24 @@ class FmgPlan:
                                          N.stream_ptr()), "plan_solve")
         return out
 
+    def solve_functional(self, forcing: torch.Tensor, weights: torch.Tensor | None = None,
+                         out: torch.Tensor | None = None) -> torch.Tensor:
+        """One FMG pass that returns, per right-hand side, J = sum_i w_i u_i
+        (``weights`` (2**m, B); None: the midpoint integral h * sum_i u_i)
+        without ever storing the finest solution (fmgsr_plan_solve_functional)."""
+        k = self.key
+        if out is None:
+            out = torch.empty(k.B, dtype=k.dtype, device=forcing.device)
+        self._check_io(forcing, forcing)
+        if weights is not None:
+            self._check_io(weights, weights)
+        if not out.is_cuda or out.dtype != k.dtype or out.numel() != k.B or not out.is_contiguous():
+            raise ValueError(f"functional output must be a contiguous {k.dtype} CUDA tensor of {k.B}")
+        N.check(N.lib().fmgsr_plan_solve_functional(
+            self._h, forcing.data_ptr(), weights.data_ptr() if weights is not None else None,
+            out.data_ptr(), N.stream_ptr()), "plan_solve_functional")
+        return out
+
     def solve_host(self, forcing: torch.Tensor, out: torch.Tensor, chunks: int,
                    inputs_ready: bool = False) -> torch.Tensor:
         """End-to-end solve from HOST memory: ``forcing`` / ``out`` are pinned CPU

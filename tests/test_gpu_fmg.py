@@ -249,3 +249,49 @@ def test_warp_coarse_kernel_matches_oracle(fm, oracle, monkeypatch, m, P, b, n_s
     for kw in (dict(), dict(coarse=m - 2), dict(coarse=5)):
         got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
         assert np.array_equal(got, want), kw
+
+
+def _ordered_functional(sol, w, W, scale):
+    """CPU restatement of the functional's summation order: per patch of W
+    owned cells a sequential sum of w*u, then a sequential sum over patches."""
+    n, B = sol.shape
+    out = []
+    for r in range(B):
+        tot = 0.0
+        for p in range(n // W):
+            acc = 0.0
+            for i in range(p * W, (p + 1) * W):
+                acc = acc + (float(w[i, r]) * float(sol[i, r]) if w is not None else float(sol[i, r]))
+            tot = tot + acc
+        out.append(tot * scale)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("m,P,b,n_sr,ns,nl,fused", [
+    (11, 64, 4, 1, 1, False, True),    # fused: the reduction rides in the final visit
+    (11, 64, 4, 0, 1, False, True),    # n_sr = 0: FAS-correction final visit
+    (11, 64, 4, 1, 1, False, False),   # unfused plan
+    (10, 16, 3, 1, 2, False, True),    # V(2,2)
+    (10, 16, 4, 1, 2, True, True),     # nonlinear
+])
+def test_functional_output_matches_ordered_sum(fm, m, P, b, n_sr, ns, nl, fused):
+    B = 8
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b, nonlinear=nl))
+    if nl:
+        f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=2))
+    else:
+        f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=5))
+    plan = fm.get_plan(fm.key_from_config(cfg, B, torch.float64, fused=fused))
+    sol = plan.solve(f).cpu().numpy()
+    W = cfg.smoother.geometry(2 ** m).W
+    g = torch.Generator(device="cuda").manual_seed(9)
+    w = torch.rand(2 ** m, B, generator=g, device="cuda", dtype=torch.float64)
+    got_w = plan.solve_functional(f, w).cpu().numpy()
+    got_h = plan.solve_functional(f).cpu().numpy()
+    assert np.array_equal(got_w, _ordered_functional(sol, w.cpu().numpy(), W, 1.0))
+    assert np.array_equal(got_h, _ordered_functional(sol, None, W, 2.0 ** -m))
+    # and it is the midpoint integral of the solution
+    assert np.allclose(got_h, sol.sum(0) / 2 ** m, rtol=1e-13, atol=0)
+    # the plain solve still works after functional graphs were captured
+    assert np.array_equal(plan.solve(f).cpu().numpy(), sol)
