@@ -33,6 +33,50 @@ __device__ __forceinline__ float xdiv(float a, float b) { return __fdiv_rn(a, b)
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
 
+// Two RHS columns per lane: V2<S> holds columns (2r, 2r+1) of a row, so a
+// warp covers 64 adjacent columns and every staged row is one 16-byte (fp64)
+// or 8-byte (fp32) access per lane.  Arithmetic is per component with the
+// same *_rn intrinsics, so each column's result is bit-identical to the
+// scalar chain; the lane simply runs two independent chains interleaved.
+template <typename S>
+struct alignas(2 * sizeof(S)) V2 {
+  S x, y;
+  V2() = default;
+  __host__ __device__ constexpr explicit V2(double v) : x((S)v), y((S)v) {}
+  __host__ __device__ constexpr V2(S a, S b) : x(a), y(b) {}
+};
+template <typename S>
+__host__ __device__ inline bool operator==(const V2<S>& a, const V2<S>& b) {
+  return a.x == b.x && a.y == b.y;
+}
+template <typename S>
+__device__ __forceinline__ V2<S> xadd(V2<S> a, V2<S> b) { return V2<S>(xadd(a.x, b.x), xadd(a.y, b.y)); }
+template <typename S>
+__device__ __forceinline__ V2<S> xsub(V2<S> a, V2<S> b) { return V2<S>(xsub(a.x, b.x), xsub(a.y, b.y)); }
+template <typename S>
+__device__ __forceinline__ V2<S> xmul(V2<S> a, V2<S> b) { return V2<S>(xmul(a.x, b.x), xmul(a.y, b.y)); }
+template <typename S>
+__device__ __forceinline__ V2<S> xdiv(V2<S> a, V2<S> b) { return V2<S>(xdiv(a.x, b.x), xdiv(a.y, b.y)); }
+// L2-coherent load (edge records written by another warp of the same launch)
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ V2<double> ldcg(const V2<double>* p) {
+  double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+  return V2<double>(v.x, v.y);
+}
+__device__ __forceinline__ V2<float> ldcg(const V2<float>* p) {
+  float2 v = __ldcg(reinterpret_cast<const float2*>(p));
+  return V2<float>(v.x, v.y);
+}
+template <typename T>
+struct LaneCols {  // RHS columns carried by one lane
+  static constexpr int value = 1;
+};
+template <typename S>
+struct LaneCols<V2<S>> {
+  static constexpr int value = 2;
+};
+
 // ---------------------------------------------------------------------------
 // Gauss-Seidel cell updates, reference _kernels_numba.py:26-35.
 //   interior : resid = f - inv_h2*((2u - uL) - uR), u += (omega*resid)/(2 inv_h2)
@@ -650,8 +694,8 @@ __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i6
     T Lr[5], Rr[5];
 #pragma unroll
     for (int k = 0; k < 5; k++) {
-      Lr[k] = __ldcg(base + k * ldE);
-      Rr[k] = __ldcg(base + (5 + k) * ldE);
+      Lr[k] = ldcg(base + k * ldE);
+      Rr[k] = ldcg(base + (5 + k) * ldE);
     }
     T fL, fR;
     edge_finish<T, NL>(Lr, Rr, inv_h2, inv_H2, fL, fR);

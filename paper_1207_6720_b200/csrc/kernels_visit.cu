@@ -16,225 +16,42 @@
 
 #include "fmgsr_chain.cuh"
 #include "fmgsr_internal.h"
+#include "visit_common.cuh"
 
 namespace fmgsr {
 
-template <typename T>
-struct VisitArgs {
-  i64 n, ld, W, b, P, nc, p_begin, qlo, qhi;
-  T* E_out;
-  bool left_remote, right_remote;
-  int B, nrg;
-  GsCoef<T> gc;
-  KzCoef<T> kz;
-  T inv_H2;
-  bool write_u;
-  const T *u_src, *uH, *uc, *f;
-  T *u_out, *uH_out, *fH_out, *E;
-  int* cnt;
-  const i64 *olo, *ohi, *elo, *ehi;
-  const T* fun_w;  // FUNC: weights (nullptr: unit)
-  T* fun_part;     // FUNC: per-(patch, column) partial sums [P][nrg * 32]
-};
-
-constexpr int VNT = 128;  // threads per block of the visit kernel
-constexpr int VD = 8;     // cp.async ring depth (pairs) per lane
-
-template <typename T, int SRC, bool CR>
-__host__ __device__ constexpr size_t visit_ring_bytes() {
-  return (size_t)VD * SrcRows<SRC, CR>::R * VNT * sizeof(T);
-}
-template <typename T, int SRC, bool CR>
-__host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one mbarrier per (warp, slot)
-  return visit_ring_bytes<T, SRC, CR>() + (size_t)(VNT / 32) * VD * 8;
-}
-
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC>
-__global__ void __launch_bounds__(VNT, 4) visit_kernel(const VisitArgs<T> a) {
-  extern __shared__ __align__(128) unsigned char visit_smem[];
-  const int lane = threadIdx.x & 31;
-  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 pl = gw / a.nrg;  // patch index within the launched range
-  const int rg = (int)(gw - pl * a.nrg);
-  if (pl >= a.P) return;  // warp-uniform
-  const i64 p = a.p_begin + pl;
-  const int r = rg * 32 + lane;
-  const bool store = r < a.B;
-  const int rr = store ? r : a.B - 1;
-
-  i64 os, oe, ws, we;
-  if (a.olo) {
-    os = a.olo[p];
-    oe = a.ohi[p];
-    ws = a.elo[p];
-    we = a.ehi[p];
-  } else {
-    os = p * a.W;
-    oe = os + a.W;
-    ws = os - a.b > 0 ? os - a.b : 0;
-    we = oe + a.b < a.n ? oe + a.b : a.n;
-  }
-
-  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD, BULK, FUNC> ch;
-  ch.lane = lane;
-  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR>()) +
-            (threadIdx.x >> 5) * VD;
-  if (BULK) {
-    if (lane == 0)
-      for (int k = 0; k < VD; k++) mbar_init(ch.bars + k, 1);
-    mbar_fence_init();
-    __syncwarp();
-  }
-  ch.src.u = a.u_src ? a.u_src + rr : nullptr;
-  ch.src.uH = a.uH ? a.uH + rr : nullptr;
-  ch.src.uc = a.uc ? a.uc + rr : nullptr;
-  ch.src.f = a.f + rr;
-  ch.src.ld = a.ld;
-  ch.src.nc = a.nc;
-  ch.src.kz = a.kz;
-  ch.src.wlo = ws >> 1;
-  ch.src.whi = we >> 1;
-  ch.src.qlo = a.qlo;
-  ch.src.qhi = a.qhi;
-  ch.gc = a.gc;
-  ch.n = a.n;
-  ch.nc = a.nc;
-  ch.ld = a.ld;
-  ch.ws = ws;
-  ch.os = os;
-  ch.oe = oe;
-  ch.store = store;
-  ch.ring = reinterpret_cast<T*>(visit_smem) + threadIdx.x;
-  ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + r : nullptr;
-  ch.fw = (FUNC && a.fun_w) ? a.fun_w + rr : nullptr;
-  ch.facc = T(0);
-  if (!EPI) {
-    ch.epi = nullptr;
-    ch.run(we);
-    if (FUNC) a.fun_part[p * ((i64)a.nrg * 32) + r] = ch.facc;
-    return;
-  }
-  Epilogue<T> ep;
-  ep.inv_h2 = a.gc.inv_h2;
-  ep.inv_H2 = a.inv_H2;
-  ep.left_dom = (os == 0);
-  ep.right_dom = (oe == a.n);
-  ep.write_uH = a.uH_out != nullptr;
-  ep.uH_out = a.uH_out ? a.uH_out + r : nullptr;
-  ep.fH_out = a.fH_out + r;
-  ep.ld = a.ld;
-  ep.nc = a.nc;
-  ep.cnt = 0;
-  ep.up2 = ep.up1 = ep.Lprev = ep.Rm2 = ep.Rm1 = ep.Rfm1 = T(0);
-  ch.epi = &ep;
-  ch.run(we);
-  EdgeRec<T> right;
-  ep.finish(store, right);
-  const i64 ldE = (i64)a.nrg * 32;
-  if (!ep.left_dom) {
-    if (pl == 0 && a.left_remote) {  // slab edge: the neighbour shard finishes it
-#pragma unroll
-      for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = ep.left.v[k];
-    } else {
-      edge_arrive(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, a.ld, os,
-                  ep.inv_h2, ep.inv_H2);
-    }
-  }
-  if (!ep.right_dom) {
-    if (pl == a.P - 1 && a.right_remote) {
-#pragma unroll
-      for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
-    } else {
-      edge_arrive(a.E, a.cnt, ldE, a.nrg, p + 1, 0, right, lane, rg, r, store, ep.fH_out, a.ld, oe,
-                  ep.inv_h2, ep.inv_H2);
-    }
-  }
-}
-
-template <typename T>
-static GsCoef<T> make_coef(i64 n, double omega) {
-  int k = level_of(n);
-  GsCoef<T> g;
-  double inv_h2 = (double)((i64)1 << (2 * k));
-  g.inv_h2 = (T)inv_h2;
-  g.rdiag = (T)(1.0 / (2.0 * inv_h2));  // exact power of two
-  g.diag_b = (T)(3.0 * inv_h2);
-  g.omega = (T)omega;
-  g.diag_i = (T)(2.0 * inv_h2);
-  return g;
-}
-
-// FMGSR_VISIT_STAGING=cpasync forces the per-lane cp.async staging (A/B tests)
-static bool visit_bulk_enabled() {
+// FMGSR_VISIT_CPL=1 forces one RHS column per lane (A/B tests)
+static bool visit_cpl2_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("FMGSR_VISIT_STAGING");
-    v = (e && std::string(e) == "cpasync") ? 0 : 1;
+    const char* e = getenv("FMGSR_VISIT_CPL");
+    v = (e && std::string(e) == "1") ? 0 : 1;
   }
   return v == 1;
 }
 
+// the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
+// compiled in parallel)
+template <typename TV, typename T>
+void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s);
+
+// Two columns per lane: whole 64-column row groups, 2-element-aligned rows
+// and pointers, uniform geometry on the whole level (no explicit patch
+// arrays, no shard slab: their edge outboxes keep the scalar layout).
+// Measured on config 2 (tools/visit_breakdown.py): mid-level visits 10-25 %
+// faster, 3.29 -> 3.08 ms per cycle; config 5 fp32 8.66 -> 6.84 ms.
 template <typename T>
-static KzCoef<T> make_kz(double pd) {
-  KzCoef<T> k;
-  int e;
-  k.proj_diag = (T)pd;
-  k.pow2 = std::frexp(pd, &e) == 0.5;  // pd = 2^(e-1): dividing is multiplying by 2^(1-e)
-  k.recip = (T)(k.pow2 ? std::ldexp(1.0, 1 - e) : 1.0 / pd);
-  return k;
-}
-
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC = false>
-static void launch_visit_k(const VisitArgs<T>& a, i64 blocks, cudaStream_t s) {
-  constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
-  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC>;
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "smem attr");
-    attr = true;
-  }
-  k<<<(unsigned)blocks, VNT, smem, s>>>(a);
-}
-
-// Bulk (TMA) staging needs whole 32-column row segments at 16-byte alignment.
-template <typename T>
-static bool bulk_ok(const VisitArgs<T>& a) {
-  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  return a.B % 32 == 0 && (a.ld * sizeof(T)) % 16 == 0 && al(a.f) &&
-         (!a.u_src || al(a.u_src)) && (!a.uH || al(a.uH)) && (!a.uc || al(a.uc)) &&
-         visit_bulk_enabled();
-}
-
-template <typename T, int SRC, bool CR, bool EPI>
-static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
-  i64 warps = a.P * a.nrg;
-  i64 blocks = (warps + VNT / 32 - 1) / (VNT / 32);
-  const bool om1 = a.gc.omega == T(1);
-  // bulk (TMA) staging pays off where per-lane LDGSTS saturates the MIO
-  // queue: sources with >= 5 staged rows per pair (the FAS-correction visits);
-  // measured slower than cp.async for 3-4 rows (profiles/r01 notes)
-  const bool bulk = SrcRows<SRC, CR>::R >= 5 && bulk_ok(a);
-  // functional output of the final up visit (non-SR: FAS correction; SR: Pi + CR)
-  if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
-    if (a.fun_part) {
-      if (om1) {
-        if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true, true>(a, blocks, s);
-        else launch_visit_k<T, SRC, CR, EPI, true, false, true>(a, blocks, s);
-      } else {
-        if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true, true>(a, blocks, s);
-        else launch_visit_k<T, SRC, CR, EPI, false, false, true>(a, blocks, s);
-      }
-      return;
-    }
-  }
-  if (om1) {
-    if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true>(a, blocks, s);
-    else launch_visit_k<T, SRC, CR, EPI, true, false>(a, blocks, s);
-  } else {
-    if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true>(a, blocks, s);
-    else launch_visit_k<T, SRC, CR, EPI, false, false>(a, blocks, s);
-  }
+static bool visit_cpl2_ok(const VisitDesc<T>& d) {
+  constexpr uintptr_t A = 2 * sizeof(T);
+  auto al = [](const void* p) { return ((uintptr_t)p & (A - 1)) == 0; };
+  // fp64 Pi + Kaczmarz (the SR up visit) measured slower with two columns per
+  // lane (U_16 of config 2: 270 vs 226 us; 16-byte lanes need ~220 registers
+  // there); every other visit kind, and every fp32 visit, is faster
+  if (sizeof(T) == 8 && d.src == SRC_FMG && d.cr) return false;
+  return visit_cpl2_enabled() && d.B % 64 == 0 && d.ld % 2 == 0 && !d.olo && d.p_count < 0 &&
+         !d.left_remote && !d.right_remote && al(d.u_src) && al(d.uH) && al(d.uc) && al(d.f) &&
+         al(d.u_out) && al(d.uH_out) && al(d.fH_out) && al(d.E) && al(d.fun_w) &&
+         al(d.fun_part);
 }
 
 template <typename T>
@@ -242,56 +59,17 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   require(d.n >= 2 && is_pow2(d.n), "visit: level size must be a power of two >= 2");
   require(d.B >= 1 && d.ld >= d.B, "visit: need 1 <= B <= ld");
   require(d.f != nullptr, "visit: f is null");
-  VisitArgs<T> a;
-  a.n = d.n;
-  a.ld = d.ld;
-  a.B = d.B;
-  a.nrg = (d.B + 31) / 32;
-  a.nc = d.n / 2;
-  a.gc = make_coef<T>(d.n, d.omega);
-  a.inv_H2 = (T)(double)((i64)1 << (2 * (level_of(d.n) - 1)));
-  a.kz = make_kz<T>(d.proj_diag);
-  a.write_u = d.write_u;
-  a.u_src = d.u_src;
-  a.uH = d.uH;
-  a.uc = d.uc;
-  a.f = d.f;
-  a.u_out = d.u_out;
-  a.uH_out = d.uH_out;
-  a.fH_out = d.fH_out;
-  a.E = d.E;
-  a.cnt = d.cnt;
-  a.olo = d.olo;
-  a.ohi = d.ohi;
-  a.elo = d.elo;
-  a.ehi = d.ehi;
-  a.p_begin = 0;
-  a.qlo = d.qlo >= 0 ? d.qlo : 0;
-  a.qhi = d.qhi >= 0 ? d.qhi : a.nc - 1;
-  a.E_out = d.E_out;
-  a.left_remote = d.left_remote;
-  a.right_remote = d.right_remote;
-  a.fun_w = d.fun_w;
-  a.fun_part = d.fun_part;
   require(!d.fun_part || (!d.epi && !d.olo && d.p_count < 0 &&
                           ((d.src == SRC_FMG && d.cr) || (d.src == SRC_CORR && !d.cr))),
           "visit: functional output only on a final up visit");
   if (d.olo) {
     require(d.src == SRC_LOAD && !d.epi, "visit: patch arrays only with plain loads");
-    a.P = d.P;
-    a.W = 0;
-    a.b = 0;
   } else {
     require(d.W >= 2 && d.W % 2 == 0 && d.n % d.W == 0, "visit: owned width must be even and divide n");
     require(d.b >= 0, "visit: negative buffer");
-    a.W = d.W;
-    a.b = d.b;
-    a.P = d.n / d.W;
-    if (d.p_count >= 0) {
-      require(d.p_begin >= 0 && d.p_begin + d.p_count <= a.P, "visit: patch range outside the level");
-      a.p_begin = d.p_begin;
-      a.P = d.p_count;
-    }
+    if (d.p_count >= 0)
+      require(d.p_begin >= 0 && d.p_begin + d.p_count <= d.n / d.W,
+              "visit: patch range outside the level");
   }
   require(!(d.left_remote || d.right_remote) || (d.E_out && d.epi), "visit: remote edges need an outbox");
   if (d.src == SRC_LOAD) require(d.u_src != nullptr, "visit: LOAD needs u_src");
@@ -304,23 +82,8 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
-  if (a.P == 0) return;
-#define FMGSR_DISPATCH(SRCV)                                                    \
-  if (d.cr) {                                                                  \
-    if (d.epi) launch_visit_t<T, SRCV, true, true>(a, s);                      \
-    else launch_visit_t<T, SRCV, true, false>(a, s);                           \
-  } else {                                                                     \
-    if (d.epi) launch_visit_t<T, SRCV, false, true>(a, s);                     \
-    else launch_visit_t<T, SRCV, false, false>(a, s);                          \
-  }
-  if (d.src == SRC_LOAD) {
-    FMGSR_DISPATCH(SRC_LOAD)
-  } else if (d.src == SRC_CORR) {
-    FMGSR_DISPATCH(SRC_CORR)
-  } else {
-    FMGSR_DISPATCH(SRC_FMG)
-  }
-#undef FMGSR_DISPATCH
+  if (visit_cpl2_ok(d)) visit_fill_launch<V2<T>>(d, s);
+  else visit_fill_launch<T>(d, s);
   check_launch("visit_kernel");
 }
 

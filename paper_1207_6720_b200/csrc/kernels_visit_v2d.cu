@@ -1,0 +1,6 @@
+// One lane type of the fused visit kernel (V2<double> lanes over double fields).
+#include "visit_impl.cuh"
+
+namespace fmgsr {
+template void visit_fill_launch<V2<double>, double>(const VisitDesc<double>&, cudaStream_t);
+}  // namespace fmgsr

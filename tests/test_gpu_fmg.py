@@ -295,3 +295,38 @@ def test_functional_output_matches_ordered_sum(fm, m, P, b, n_sr, ns, nl, fused)
     assert np.allclose(got_h, sol.sum(0) / 2 ** m, rtol=1e-13, atol=0)
     # the plain solve still works after functional graphs were captured
     assert np.array_equal(plan.solve(f).cpu().numpy(), sol)
+
+
+@pytest.mark.parametrize("m,P,b,n_sr", [(12, 64, 4, 1), (12, 64, 4, 0), (12, 16, 1, 2),
+                                        (12, 1024, 8, 1), (11, 4, 3, 1)])
+def test_two_column_lanes_match_oracle(fm, oracle, m, P, b, n_sr):
+    """B a multiple of 64: the visit kernels run two RHS columns per lane
+    (V2 lanes); bit for bit against the oracle on every column, and the
+    functional output reduces the same bits."""
+    B = 128
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=P, buffer=b))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + 7 * b + P))
+    want = oracle.fmg_solve_batch(oracle_cfg(oracle, cfg), np.ascontiguousarray(f.cpu().numpy().T),
+                                  nthreads=8).T
+    for kw in (dict(), dict(fused=False), dict(coarse=0)):
+        got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
+        assert np.array_equal(got, want), kw
+    plan = fm.get_plan(fm.key_from_config(cfg, B, torch.float64))
+    W = cfg.smoother.geometry(2 ** m).W
+    got_h = plan.solve_functional(f).cpu().numpy()
+    assert np.array_equal(got_h, _ordered_functional(want, None, W, 2.0 ** -m))
+
+
+def test_two_column_lanes_fp32_match_scalar_lanes(fm):
+    """fp32: a batch of 64 (two columns per lane) equals the same columns
+    solved as two batches of 32 (one column per lane), bit for bit."""
+    m = 12
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=64, buffer=4))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(64, seed=17))
+    f = f.float()
+    whole = fm.fmg_solve(cfg, f)[0]
+    halves = torch.cat([fm.fmg_solve(cfg, f[:, :32].contiguous())[0],
+                        fm.fmg_solve(cfg, f[:, 32:].contiguous())[0]], dim=1)
+    assert torch.equal(whole, halves)
