@@ -20,8 +20,11 @@ prof() {  # name workload kernel-regex skip
   [ "${KEEP_REPS:-0}" = "1" ] || rm -f "$OUT/$1.ncu-rep"  # gpurun copies back <= 64 MiB
 }
 profiles() {
-  prof T16 config2 "visit_kernel<double, .int.2, .bool.0, .bool.1, .bool.1, .bool.0>" 6
-  prof U16 config2 "visit_kernel<double, .int.2, .bool.1, .bool.0, .bool.1, .bool.0>" 0
+  # config 2 finest visits: T_16 runs two RHS columns per lane (V2<double>),
+  # U_16 (Pi + Kaczmarz) one; U_11 is a mid-level FAS-correction visit (V2)
+  prof T16 config2 "visit_kernel<fmgsr::V2<double>, .int.2, .bool.0, .bool.1, .bool.1, .bool.0, .bool.0>" 6
+  prof U16 config2 "visit_kernel<double, .int.2, .bool.1, .bool.0, .bool.1, .bool.0, .bool.0>" 0
+  prof U11 config2 "visit_kernel<fmgsr::V2<double>, .int.1, .bool.0, .bool.0, .bool.1, .bool.0, .bool.0>" 2
   prof T20 config3 "ns2_kernel<double, .int.2, .bool.0, .bool.1, .bool.1, .bool.1>" 10
   prof U20 config3 "ns2_kernel<double, .int.2, .bool.1, .bool.1, .bool.1, .bool.0>" 0
 }

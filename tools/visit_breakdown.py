@@ -1,7 +1,7 @@
 """Per-level-visit device times of one FMG pass (op-by-op launches with CUDA
 events on the launching stream), summed by level and kind.
 
-    python tools/visit_breakdown.py [--workload config2] [--reps 3] [--unfused]
+    python tools/visit_breakdown.py [--workload config2] [--reps 3] [--unfused] [--B 128]
 """
 import argparse
 import collections
@@ -19,8 +19,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="config2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--unfused", action="store_true")
+ap.add_argument("--B", type=int, default=0, help="override the workload's batch size")
 a = ap.parse_args()
-w = bench.WORKLOADS[a.workload]
+w = dict(bench.WORKLOADS[a.workload])
+if a.B:
+    w["B"] = a.B
 dt = torch.float64 if w["dtype"] == "f64" else torch.float32
 nl = bool(w.get("nonlinear", False))
 cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
