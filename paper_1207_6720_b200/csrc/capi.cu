@@ -119,6 +119,7 @@ struct Plan : PlanBase {
   // coarse hierarchy kernel: levels m0..Lc on chip, CW RHS columns per CTA
   bool use_coarse = false, coarse_warp = true;
   int Lc = 0, CW = 1;
+  int CNW = 1;  // warp kernel: warps per column (one chain per thread on level Lc)
   int coarse_trace = 0;
   // patch-slab sharding: levels > Lr are split into S slabs, this is slab srank;
   // slab arrays carry H halo rows per side and are addressed through
@@ -183,21 +184,29 @@ struct Plan : PlanBase {
       check_cuda(cudaGetDevice(&dev), "device");
       check_cuda(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem/SM");
       check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
+      // warps per column: one chain per thread on the deepest level (a
+      // thread's serial work grows with P_l / (32 NW)), at most 8 warps
+      auto nw_for = [&](int lc) {
+        int nw = 1;
+        while (nw < 8 && 32 * nw < lv[lc].n / lv[lc].W) nw *= 2;
+        return nw;
+      };
+      int max_nw = 8;
+      if (const char* e = getenv("FMGSR_COARSE_NW")) max_nw = atoi(e);
       auto fits = [&](int lc) {
         CoarseArgs<T> t;
         t.m0 = m0;
         t.Lc = lc;
+        t.nw = nw_for(lc);
+        if (t.nw > max_nw || 32 * t.nw < lv[lc].n / lv[lc].W) return false;
         for (int l = m0; l <= lc; l++) {
           t.W[l] = lv[l].W;
           t.b[l] = lv[l].b;
         }
         const size_t bytes = coarse_warp_layout(t, d.ns == 2, d.nonlinear != 0);
         if (bytes > 227 * 1024) return false;
-        // one chain per lane: a warp's serial work grows with P_l / 32
-        // (config 3: Lc = 6 measured best against 8..11)
-        if (lv[lc].n / lv[lc].W > 32) return false;
         i64 per_sm = (i64)smsm / (i64)(bytes + 1024);
-        if (per_sm > 32) per_sm = 32;
+        if (per_sm > 64 / t.nw) per_sm = 64 / t.nw;
         return per_sm >= 1 && per_sm * nsm >= d.B;
       };
       while (Lc + 1 <= m - 1 && fits(Lc + 1)) Lc++;
@@ -205,6 +214,7 @@ struct Plan : PlanBase {
       if (want < 0)
         if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
       if (want > 0 && want - 1 >= m0 && want - 1 < Lc) Lc = want - 1;
+      CNW = nw_for(Lc);
     } else if (use_coarse) {
       i64 cw = 1;
       // ~128 CTAs (one wave on 148 SMs); measured best against 256 / 512
@@ -731,6 +741,7 @@ struct Plan : PlanBase {
     a.n_sr = d.n_sr;
     a.mode = mode;
     a.CW = CW;
+    a.nw = CNW;
     a.B = (int)d.B;
     a.ld = d.ld;
     for (int l = d.m0; l <= Lc; l++) {

@@ -81,6 +81,7 @@ struct CoarseArgs {
   // warp-per-column kernel layout (filled by coarse_warp_layout)
   int lgW[32] = {}, off[32] = {}, slen[32] = {};
   int fields = 0, scratch = 0;
+  int nw = 1;  // warps per column (coarse_warp_kernel)
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
 template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW);

@@ -1,11 +1,12 @@
 // kernels_coarse_warp.cu -- the coarse end of the hierarchy, one warp per RHS.
 //
 // Below the cutoff Lc every level visit is microseconds of latency-bound work.
-// Right-hand sides are independent, so each warp owns ONE column and runs all
-// visits of levels m0..Lc for it out of its own slice of shared memory; the 32
-// lanes split each phase (patch chains, restriction rows, prolongation rows)
-// and phases are separated by __syncwarp() only -- no CTA barriers, so the
-// warps resident on an SM never wait for one another.
+// Right-hand sides are independent, so each CTA of NW warps (NW = 1, 2, 4, 8)
+// owns ONE column and runs all visits of levels m0..Lc for it out of its own
+// slice of shared memory; the 32 NW threads split each phase (patch chains,
+// restriction rows, prolongation rows), one chain per thread on the deepest
+// level, and phases are separated by __syncwarp() (NW = 1) or a barrier of
+// the column's own CTA -- columns never wait for one another.
 //   mode 0 (coarse FMG): the coarsest solve and FMG steps m0+1..Lc
 //                        (reference cycles.py:178-199 for those levels);
 //   mode 1 (V segment) : for a step t > Lc, the part of its V-cycle below
@@ -33,14 +34,15 @@ namespace {
 
 __device__ __forceinline__ double p2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
-template <typename T, bool NS2, bool NL>
+template <typename T, bool NS2, bool NL, int NW>
 struct Warp {
+  static constexpr int NT = 32 * NW;  // threads per column
   const CoarseArgs<T>& a;
   T* base;      // this warp's slice
   T* scr;       // ns2 scratch (per chain 2b+2 cells, lane-strided) / Newton work
   T* dfac;      // linear direct factor d[n0], e[n0]
   T* efac;
-  int lane;
+  int lane;  // thread index within the column's CTA (0 .. NT-1)
   unsigned curmask;
   __device__ Warp(const CoarseArgs<T>& args) : a(args) {}
 
@@ -51,7 +53,10 @@ struct Warp {
   __device__ __forceinline__ int cur(int l) const { return (curmask >> l) & 1; }
   __device__ __forceinline__ void flip(int l) { curmask ^= 1u << l; }
   __device__ __forceinline__ bool sr(int l) const { return l > a.m - a.n_sr; }
-  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ void sync() const {
+    if (NW == 1) __syncwarp();
+    else __syncthreads();
+  }
 
   __device__ GsCoef<T> coef(int l) const {
     GsCoef<T> gc;
@@ -66,14 +71,14 @@ struct Warp {
   // ---- global <-> shared (one column, padded layout) --------------------------
   __device__ void load(T* dst, const T* src, int l) {
     const int n = N(l);
-    for (int i = lane; i < n; i += 32) cp_async(dst + pd(l, i), src + (i64)i * a.ld);
+    for (int i = lane; i < n; i += NT) cp_async(dst + pd(l, i), src + (i64)i * a.ld);
     cp_commit();
     cp_wait<0>();
     sync();
   }
   __device__ void store(T* dst, const T* src, int l) {
     const int n = N(l);
-    for (int i = lane; i < n; i += 32) dst[(i64)i * a.ld] = src[pd(l, i)];
+    for (int i = lane; i < n; i += NT) dst[(i64)i * a.ld] = src[pd(l, i)];
   }
 
   // ---- prologue sources (value of the smoother input at fine cell x) ----------
@@ -142,7 +147,10 @@ struct Warp {
     return (x & 1) ? q : p;
   }
   __device__ __forceinline__ T gs(const GsCoef<T>& gc, int i, int n, T uL, T u, T uR, T f) const {
-    return NL ? gs_cell_nl(gc, i, n, uL, u, uR, f) : gs_cell(gc, i, n, uL, u, uR, f);
+    if (!NL) return gs_cell(gc, i, n, uL, u, uR, f);
+    // interior Newton step with 1/J off the uL dependency (bitwise the IEEE quotient)
+    if (i > 0 && i < n - 1) return gs_int_nl<T, false>(gc, uL, u, uR, f);
+    return gs_cell_nl(gc, i, n, uL, u, uR, f);
   }
 
   // ---- patch smoother: out (level l) = S(input given by SRC / CR) -------------------
@@ -150,7 +158,7 @@ struct Warp {
   __device__ void smooth(int l, const T* u, const T* uH, const T* f, T* out) {
     const int n = N(l), W = (int)a.W[l], b = (int)a.b[l], P = n / W;
     const GsCoef<T> gc = coef(l);
-    for (int p = lane; p < P; p += 32) {
+    for (int p = lane; p < P; p += NT) {
       const int os = p * W, oe = os + W;
       const int ws = os - b > 0 ? os - b : 0;
       const int we = oe + b < n ? oe + b : n;
@@ -181,15 +189,15 @@ struct Warp {
           const T nn = i + 2 < n ? val<SRC, CR>(l, u, uH, i + 2, wlo, whi) : T(0);
           const T v = gs(gc, i, n, uL, cu, nx, f[pd(l, i)]);
           if (i >= os && i < oe) out[pd(l, i)] = v;
-          else sc[32 * sidx(i)] = v;
+          else sc[NT * sidx(i)] = v;
           uL = v;
           cu = nx;
           nx = nn;
         }
-        if (we < n) sc[32 * (1 + nl + nr)] = cu;  // raw value of we (pair we/2 never projected)
+        if (we < n) sc[NT * (1 + nl + nr)] = cu;  // raw value of we (pair we/2 never projected)
         // backward: second Kaczmarz pass on the forward values, just in time
         auto fv = [&](int x) -> T {
-          return (x >= os && x < oe) ? out[pd(l, x)] : x >= we ? sc[32 * (1 + nl + nr)] : sc[32 * sidx(x)];
+          return (x >= os && x < oe) ? out[pd(l, x)] : x >= we ? sc[NT * (1 + nl + nr)] : sc[NT * sidx(x)];
         };
         auto fv2 = [&](int x) -> T {  // pass-2 value of x (its pair projected if in range)
           if (!CR) return fv(x);
@@ -228,7 +236,7 @@ struct Warp {
       if (NL) v = xadd(v, cube(U_(i)));
       return v;
     };
-    for (int j = lane; j < nc; j += 32) {
+    for (int j = lane; j < nc; j += NT) {
       const T Rj = ru(j);
       T LH;
       if (j == 0) LH = xmul(xsub(xmul(T(3), Rj), ru(1)), iH);
@@ -326,11 +334,11 @@ struct Warp {
   }
 };
 
-template <typename T, bool NS2, bool NL>
-__global__ void __launch_bounds__(32) coarse_warp_kernel(const __grid_constant__ CoarseArgs<T> a) {
+template <typename T, bool NS2, bool NL, int NW>
+__global__ void __launch_bounds__(32 * NW) coarse_warp_kernel(const __grid_constant__ CoarseArgs<T> a) {
   extern __shared__ __align__(16) unsigned char cw_smem[];
   const int r = blockIdx.x;  // this warp's RHS column
-  Warp<T, NS2, NL> w(a);
+  Warp<T, NS2, NL, NW> w(a);
   w.lane = threadIdx.x;
   w.base = reinterpret_cast<T*>(cw_smem);
   w.scr = w.base + a.fields;
@@ -392,7 +400,7 @@ size_t coarse_warp_layout(CoarseArgs<T>& a, bool ns2, bool nl) {
     a.off[l] = (int)off;
     off += 3 * len;
     if (ns2 && l > a.m0) {
-      const i64 s = 32 * (2 * a.b[l] + 2);
+      const i64 s = 32 * (i64)a.nw * (2 * a.b[l] + 2);
       if (s > scratch) scratch = s;
     }
   }
@@ -428,15 +436,30 @@ void launch_coarse_warp(const CoarseArgs<T>& args, bool ns2, bool nl, cudaStream
       g = it->second;
     }
     require(smem <= (size_t)g, "coarse: shared memory budget exceeded");
-    kf<<<(unsigned)a.B, 32, smem, s>>>(a);
+    kf<<<(unsigned)a.B, 32 * a.nw, smem, s>>>(a);
   };
-  if (ns2) {
-    if (nl) go(coarse_warp_kernel<T, true, true>);
-    else go(coarse_warp_kernel<T, true, false>);
-  } else {
-    if (nl) go(coarse_warp_kernel<T, false, true>);
-    else go(coarse_warp_kernel<T, false, false>);
+#define CWK_NW(NS, NLV)                                      \
+  switch (a.nw) {                                            \
+    case 1: go(coarse_warp_kernel<T, NS, NLV, 1>); break;    \
+    case 2: go(coarse_warp_kernel<T, NS, NLV, 2>); break;    \
+    case 4: go(coarse_warp_kernel<T, NS, NLV, 4>); break;    \
+    case 8: go(coarse_warp_kernel<T, NS, NLV, 8>); break;    \
+    default: require(false, "coarse: warps per column must be 1, 2, 4 or 8"); \
   }
+  if (ns2) {
+    if (nl) {
+      CWK_NW(true, true)
+    } else {
+      CWK_NW(true, false)
+    }
+  } else {
+    if (nl) {
+      CWK_NW(false, true)
+    } else {
+      CWK_NW(false, false)
+    }
+  }
+#undef CWK_NW
   check_launch("coarse_warp_kernel");
 }
 
