@@ -53,9 +53,18 @@ struct Warp {
   __device__ __forceinline__ int cur(int l) const { return (curmask >> l) & 1; }
   __device__ __forceinline__ void flip(int l) { curmask ^= 1u << l; }
   __device__ __forceinline__ bool sr(int l) const { return l > a.m - a.n_sr; }
-  __device__ __forceinline__ void sync() const {
+  // FMGSR_COARSE_TRACE=1: thread 0 of CTA 0 stamps the clock at every phase
+  // barrier and prints the deltas at exit (phase-latency profiling)
+  long long* ts = nullptr;
+  int nts = 0;
+  __device__ __forceinline__ void sync() {
     if (NW == 1) __syncwarp();
     else __syncthreads();
+    if (ts && lane == 0 && nts < 128) ts[nts++] = clock64();
+  }
+  __device__ void dump() const {
+    if (ts && lane == 0)
+      for (int i = 1; i < nts; i++) printf("coarse-warp-trace %d %lld\n", i, ts[i] - ts[i - 1]);
   }
 
   __device__ GsCoef<T> coef(int l) const {
@@ -147,10 +156,9 @@ struct Warp {
     return (x & 1) ? q : p;
   }
   __device__ __forceinline__ T gs(const GsCoef<T>& gc, int i, int n, T uL, T u, T uR, T f) const {
-    if (!NL) return gs_cell(gc, i, n, uL, u, uR, f);
-    // interior Newton step with 1/J off the uL dependency (bitwise the IEEE quotient)
-    if (i > 0 && i < n - 1) return gs_int_nl<T, false>(gc, uL, u, uR, f);
-    return gs_cell_nl(gc, i, n, uL, u, uR, f);
+    // (the split-division interior Newton step, gs_int_nl, measured slower here:
+    //  247 vs 227 us per V segment at config 3)
+    return NL ? gs_cell_nl(gc, i, n, uL, u, uR, f) : gs_cell(gc, i, n, uL, u, uR, f);
   }
 
   // ---- patch smoother: out (level l) = S(input given by SRC / CR) -------------------
@@ -340,6 +348,8 @@ __global__ void __launch_bounds__(32 * NW) coarse_warp_kernel(const __grid_const
   const int r = blockIdx.x;  // this warp's RHS column
   Warp<T, NS2, NL, NW> w(a);
   w.lane = threadIdx.x;
+  __shared__ long long ts_s[128];
+  if (a.trace && blockIdx.x == 0) w.ts = ts_s;
   w.base = reinterpret_cast<T*>(cw_smem);
   w.scr = w.base + a.fields;
   w.dfac = w.scr + a.scratch;
@@ -379,6 +389,8 @@ __global__ void __launch_bounds__(32 * NW) coarse_warp_kernel(const __grid_const
     for (int l = m0 + 1; l <= Lc; l++) w.visit_up(l);
   }
   w.store(a.u_top + col, w.U(Lc, w.cur(Lc)), Lc);
+  w.sync();
+  w.dump();
 }
 
 }  // namespace
@@ -429,6 +441,9 @@ void launch_coarse_warp(const CoarseArgs<T>& args, bool ns2, bool nl, cudaStream
         check_cuda(cudaGetDevice(&dev), "coarse device");
         check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
                    "coarse smem optin");
+        cudaFuncAttributes fa;
+        check_cuda(cudaFuncGetAttributes(&fa, kf), "coarse func attrs");
+        optin -= (int)fa.sharedSizeBytes;  // the static trace stamps
         check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin),
                    "coarse smem attr");
         it = granted.emplace((const void*)kf, optin).first;
