@@ -51,6 +51,9 @@ def reduce_max(x: float, world: int, device: str = "cuda") -> float:
     import torch
     import torch.distributed as dist
 
+    if dist.get_backend() == "gloo":
+        device = "cpu"
+
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -229,9 +232,17 @@ def run_gpu(args, w):
     import paper_1207_6720_b200 as fm
 
     world, rank, local = dist_env()
+    # FMGSR_BENCH_BACKEND=gloo: functional check of the multi-rank plumbing with
+    # several ranks on fewer GPUs (never a reported measurement: ranks share SMs)
+    backend = os.environ.get("FMGSR_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dtype = torch.float64 if w["dtype"] == "f64" else torch.float32
     m, B = w["m"], w["B"]
     n = 2 ** m

@@ -176,7 +176,10 @@ struct Chain {
   __device__ __forceinline__ void run(i64 we) {
     const i64 qs = (ws > 0) ? ((ws - 1) >> 1) : 0;
     const i64 qe = (oe - 1) >> 1;
-    // chain head: state before pair qs, pair qs itself, then D-1 staged pairs
+    // chain head: the D-1 staged pairs are issued first so their latency
+    // overlaps the direct loads of the state before pair qs and of pair qs
+    x0 = qs + 1;
+    for (int k = 1; k < D; k++) stage(qs + k);
     src.init(qs);
     {
       Raw<T> r = src.load(qs);
@@ -184,8 +187,6 @@ struct Chain {
       f0 = r.f0;
       f1 = r.f1;
     }
-    x0 = qs + 1;
-    for (int k = 1; k < D; k++) stage(qs + k);
     uL = T(0);
     // interior range: both cells updated and interior, generation of q+1
     // interior, CR window interior, unclamped fast issue of q + D
