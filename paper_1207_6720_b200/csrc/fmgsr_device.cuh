@@ -178,6 +178,14 @@ __device__ __forceinline__ T div_by(T x, T J, T y) {
   return q;
 }
 
+// two-column lanes: the split division per component
+template <typename S>
+__device__ __forceinline__ V2<S> xrcp(V2<S> J) { return V2<S>(xrcp(J.x), xrcp(J.y)); }
+template <typename S>
+__device__ __forceinline__ V2<S> div_by(V2<S> x, V2<S> J, V2<S> y) {
+  return V2<S>(div_by(x.x, J.x, y.x), div_by(x.y, J.y, y.y));
+}
+
 // Interior nonlinear GS cell (gs_cell_nl, i not a domain row) with the
 // division split: J and 1/J depend only on the old u, so they are computed
 // ahead of the uL dependency.

@@ -105,3 +105,23 @@ def test_ns2_omega_matches_oracle(fm, oracle, nonlinear):
     want = oracle.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=8).T
     got = fm.fmg_solve(cfg, f)[0].cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("nonlinear", [True, False])
+def test_ns2_two_column_lanes_match_oracle(fm, oracle, nonlinear):
+    """V(2,2) with B = 64 and long chains (W >= 256 on levels 10-12): the
+    FAS-correction visits run two RHS columns per lane; every column bit for
+    bit against the oracle."""
+    m, P, b, B = 12, 4, 4, 64
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=2, n_patches=P, buffer=b,
+                                                     nonlinear=nonlinear))
+    if nonlinear:
+        f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=4))
+    else:
+        f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=4))
+    oc = oracle.make_cfg(3, m, 1, 2, oracle.GEOM_PATCHES, P, b, nonlin=nonlinear)
+    want = oracle.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=8).T
+    for kw in (dict(), dict(coarse=0)):
+        got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
+        assert np.array_equal(got, want), kw
