@@ -118,6 +118,9 @@ struct Plan : PlanBase {
   bool timing = false;
   // coarse hierarchy kernel: levels m0..Lc on chip, CW RHS columns per CTA
   bool use_coarse = false, coarse_warp = true;
+  // whole solve on chip (Lc = m): every level, the finest included, in one
+  // coarse launch after the f cascade
+  bool whole = false;
   int Lc = 0, CW = 1;
   int CNW = 1;  // warp kernel: warps per column (one chain per thread on level Lc)
   int coarse_trace = 0;
@@ -228,6 +231,21 @@ struct Plan : PlanBase {
       if (want < 0)
         if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
       if (want > 0 && want - 1 >= m0 && want - 1 < Lc) Lc = want - 1;
+      // Whole solve on chip when every level fits and the column groups fill at
+      // most one wave (small batches, e.g. config 1: one RHS, N = 2^10): the
+      // finest visits then run from shared memory too and a solve is two
+      // launches (auto, or coarse = m + 1; FMGSR_COARSE_WHOLE=0 disables).
+      const char* we = getenv("FMGSR_COARSE_WHOLE");
+      const bool allow = !(we && we[0] == '0');
+      int dev = 0, nsm = 0;
+      check_cuda(cudaGetDevice(&dev), "device");
+      check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
+      const bool fits = coarse_smem_bytes<T>(m0, m, CW) <= 200 * 1024 &&
+                        (d.B + CW - 1) / CW <= nsm;
+      if (S == 1 && fits && ((want < 0 && allow) || want == m + 1)) {
+        whole = true;
+        Lc = m;
+      }
     }
     if (S > 1) {
       plan_shards(Bp);
@@ -773,7 +791,7 @@ struct Plan : PlanBase {
       st.push_back({ST_CASCADE_HI, d.m, 0});
     }
     st.push_back({ST_CASCADE_LO, d.m, 0});
-    st.push_back({ST_COARSE_FMG, Lc, 0});
+    st.push_back({ST_COARSE_FMG, Lc, 0});  // whole: Lc = m, the loop below is empty
     for (int t = Lc + 1; t <= d.m; t++) {
       st.push_back({ST_TOP, t, t});
       for (int l = t - 1; l > Lc; l--) st.push_back({ST_DOWN, l, t});
@@ -827,8 +845,19 @@ struct Plan : PlanBase {
         mark_begin(s, Lc, VK_COARSE);
         CoarseArgs<T> a = coarse_args(0);
         a.u_top = lv[Lc].u[lv[Lc].cur];
+        if (whole) {  // the caller's forcing in, the finest solution out
+          a.forig[d.m] = forcing;
+          a.u_top = (solution && !fun_mode) ? solution : lv[d.m].u[0];
+        }
         launch_coarse_any(a, s);
         n_launch++;
+        if (whole && fun_mode) {  // the same ordered reduction as the fused visit
+          const Level& L = lv[d.m];
+          const T scale = fun_w ? T(1) : (T)std::ldexp(1.0, -d.m);
+          launch_functional_field(lv[d.m].u[0], fun_w, L.n, L.W, d.ld, (int)d.B, fun_part, s);
+          launch_functional_reduce(fun_part, L.n / L.W, (int)d.B, scale, fun_out, s);
+          n_launch += 2;
+        }
         mark_end(s);
         break;
       }

@@ -64,18 +64,30 @@ struct CoarseCtx {
   // barrier between phases; FMGSR_COARSE_TRACE=1 makes CTA 0 printf the
   // clock at every barrier (phase-latency profiling, off by default)
   int nbar;
-  __device__ __forceinline__ long long* tstamp() const {
-    __shared__ long long ts[96];
-    return ts;
+  struct Trace {
+    long long t[256];
+    const char* what[256];
+    int lvl[256];
+  };
+  __device__ __forceinline__ Trace* trace() const {
+    __shared__ Trace tr;
+    return &tr;
   }
   __device__ __forceinline__ void bar(const char* what, int l) {
     __syncthreads();
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < 96) tstamp()[nbar++] = clock64();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < 256) {
+      Trace* tr = trace();
+      tr->t[nbar] = clock64();
+      tr->what[nbar] = what;
+      tr->lvl[nbar++] = l;
+    }
   }
   __device__ void dump() {
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0)
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      const Trace* tr = trace();
       for (int i = 1; i < nbar; i++)
-        printf("coarse-trace %d %lld\n", i, tstamp()[i] - tstamp()[i - 1]);
+        printf("coarse-trace %d %lld %s %d\n", i, tr->t[i] - tr->t[i - 1], tr->what[i], tr->lvl[i]);
+    }
   }
 
   // global -> shared by cp.async: every element in flight at once, one wait

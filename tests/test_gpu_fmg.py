@@ -78,7 +78,7 @@ def test_fmg_batch_matches_oracle(fm, oracle, m, P, b, n_sr, ns):
                                   nthreads=8).T
     variants = {"auto": dict(), "unfused": dict(fused=False), "no_coarse": dict(coarse=0),
                 "coarse_m0": dict(coarse=4), "coarse_mid": dict(coarse=m - 3),
-                "coarse_all": dict(coarse=m)}
+                "coarse_all": dict(coarse=m), "whole_on_chip": dict(coarse=m + 1)}
     for name, kw in variants.items():
         got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
         assert np.array_equal(got, want), name
