@@ -188,7 +188,10 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   // measured slower than cp.async for 3-4 rows (profiles/r01 notes), and for
   // short chains (owned width < 64: levels 10-11 of config 2, where the lane-0
   // issue of five bulk copies per pair sits on the critical path)
-  const bool bulk = SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && bulk_ok(a);
+  // fp32 lanes (128 / 256-byte row segments) measured faster with cp.async on
+  // every visit (config 5 fp32: level-19 up 452 -> 379 us)
+  constexpr bool fp64_lanes = sizeof(T) == 8 * LaneCols<T>::value;
+  const bool bulk = fp64_lanes && SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && bulk_ok(a);
   // functional output of the final up visit (non-SR: FAS correction; SR: Pi + CR)
   if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
     if (a.fun_part) {
