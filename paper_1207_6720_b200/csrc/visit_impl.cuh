@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "fmgsr_chain.cuh"
 #include "fmgsr_internal.h"
@@ -188,10 +189,12 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   // measured slower than cp.async for 3-4 rows (profiles/r01 notes), and for
   // short chains (owned width < 64: levels 10-11 of config 2, where the lane-0
   // issue of five bulk copies per pair sits on the critical path)
-  // fp32 lanes (128 / 256-byte row segments) measured faster with cp.async on
-  // every visit (config 5 fp32: level-19 up 452 -> 379 us)
-  constexpr bool fp64_lanes = sizeof(T) == 8 * LaneCols<T>::value;
-  const bool bulk = fp64_lanes && SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && bulk_ok(a);
+  // Bulk copies only for scalar fp64 lanes: with two columns per lane (the
+  // default for B % 64 == 0) per-lane 16-byte cp.async measured faster on
+  // every config (config 2 / 4 / 5: +0.3 / +1.5 / +1.6 % per cycle), and fp32
+  // lanes likewise (config 5 fp32: level-19 up 452 -> 379 us)
+  constexpr bool bulk_lanes = std::is_same<T, double>::value;
+  const bool bulk = bulk_lanes && SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && bulk_ok(a);
   // functional output of the final up visit (non-SR: FAS correction; SR: Pi + CR)
   if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
     if (a.fun_part) {
