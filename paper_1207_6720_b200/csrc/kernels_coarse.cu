@@ -44,8 +44,9 @@ template <typename T, int CW>
 struct CoarseCtx {
   const CoarseArgs<T>& a;
   T* sm;
-  const T* dfac;  // direct-solve factor d[n0], e[n0]
+  const T* dfac;  // direct-solve factor d[n0], e[n0], RN(1/d)[n0]
   const T* efac;
+  const T* rfac;
   int c0;
   unsigned curmask;
   __device__ CoarseCtx(const CoarseArgs<T>& args) : a(args) {}
@@ -271,10 +272,12 @@ struct CoarseCtx {
         prev = xsub(f[i * CW + c], xmul(prev, efac[i - 1]));
         u[i * CW + c] = prev;
       }
-      T nx = xdiv(prev, dfac[n - 1]);
+      // x / d[i] as div_by with the reciprocals of the (constant) factor:
+      // bitwise the IEEE quotient, and off the backward recurrence's chain
+      T nx = div_by(prev, dfac[n - 1], rfac[n - 1]);
       u[(n - 1) * CW + c] = nx;
       for (int i = n - 2; i >= 0; i--) {
-        nx = xsub(xdiv(u[i * CW + c], dfac[i]), xmul(nx, efac[i]));
+        nx = xsub(div_by(u[i * CW + c], dfac[i], rfac[i]), xmul(nx, efac[i]));
         u[i * CW + c] = nx;
       }
     }
@@ -345,9 +348,11 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
       e[i] = xdiv(ei, d[i]);
       d[i + 1] = xsub(d[i + 1], xmul(e[i], ei));
     }
+    for (int i = 0; i < n0; i++) e[n0 + i] = xrcp(d[i]);
   }
   x.dfac = d;
   x.efac = e;
+  x.rfac = e + n0;
   if (a.mode == 0) {
     x.load(x.Fl(m0), a.forig[m0], n0);
     x.bar("load", m0);
@@ -409,7 +414,7 @@ template <typename T>
 size_t coarse_smem_bytes(int m0, int Lc, int CW) {
   i64 cells = 0;
   for (int l = m0; l <= Lc; l++) cells += (i64)1 << l;
-  return (size_t)(3 * cells * CW + 2 * ((i64)1 << m0)) * sizeof(T);
+  return (size_t)(3 * cells * CW + 3 * ((i64)1 << m0)) * sizeof(T);
 }
 
 template <typename T, int CW>
