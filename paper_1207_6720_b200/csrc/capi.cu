@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
+#include <mutex>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -25,6 +26,27 @@
 #include "fmgsr_internal.h"
 
 namespace fmgsr {
+
+int smem_optin(const void* kf) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> granted;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "smem opt-in device");
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, kf);
+  auto it = granted.find(key);
+  if (it != granted.end()) return it->second;
+  int optin = 0;
+  check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
+             "smem opt-in limit");
+  cudaFuncAttributes fa;
+  check_cuda(cudaFuncGetAttributes(&fa, kf), "kernel attributes");
+  const int g = optin - (int)fa.sharedSizeBytes;
+  check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, g),
+             "smem opt-in");
+  granted.emplace(key, g);
+  return g;
+}
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }

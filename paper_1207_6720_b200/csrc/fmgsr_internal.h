@@ -33,6 +33,12 @@ inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(ERR_ARG, msg);
 }
 
+// Opt kernel `kf` into the device's full dynamic shared memory (the opt-in
+// limit minus the kernel's static shared memory) on the CURRENT device --
+// function attributes live per device context -- once per (device, kernel);
+// returns the granted bytes (capi.cu).
+int smem_optin(const void* kf);
+
 __host__ __device__ inline int level_of(i64 n) {
   int k = 0;
   while (((i64)1 << (k + 1)) <= n) k++;

@@ -419,19 +419,7 @@ size_t coarse_smem_bytes(int m0, int Lc, int CW) {
 
 template <typename T, int CW>
 static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s) {
-  static int granted = -1;  // dynamic smem opted in for this instantiation
-  if (granted < 0) {
-    int dev = 0, optin = 0;
-    check_cuda(cudaGetDevice(&dev), "coarse device");
-    check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
-               "coarse smem optin");
-    cudaFuncAttributes fa;
-    check_cuda(cudaFuncGetAttributes(&fa, coarse_kernel<T, CW>), "coarse attrs");
-    granted = optin - (int)fa.sharedSizeBytes;
-    check_cuda(cudaFuncSetAttribute(coarse_kernel<T, CW>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, granted),
-               "coarse smem attr");
-  }
+  const int granted = smem_optin((const void*)coarse_kernel<T, CW>);
   require(smem <= (size_t)granted, "coarse: shared memory budget exceeded");
   unsigned blocks = (unsigned)((a.B + CW - 1) / CW);
   coarse_kernel<T, CW><<<blocks, CNT, smem, s>>>(a);

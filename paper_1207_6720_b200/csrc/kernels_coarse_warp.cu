@@ -22,8 +22,6 @@
 // the grid kernels, so results stay bit-identical to the reference / oracle.
 #include <cmath>
 #include <cstdio>
-#include <map>
-#include <mutex>
 
 #include "fmgsr_device.cuh"
 #include "fmgsr_internal.h"
@@ -428,28 +426,8 @@ void launch_coarse_warp(const CoarseArgs<T>& args, bool ns2, bool nl, cudaStream
   require(a.Lc >= a.m0 && a.Lc < 31, "coarse: bad cutoff");
   const size_t smem = coarse_warp_layout(a, ns2, nl);
   require(smem <= 227 * 1024, "coarse: shared memory budget exceeded");
-  // (all variants share one function-pointer type: opt in per kernel address)
-  static std::mutex mu;
-  static std::map<const void*, int> granted;
   auto go = [&](void (*kf)(const CoarseArgs<T>)) {
-    int g;
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      auto it = granted.find((const void*)kf);
-      if (it == granted.end()) {
-        int dev = 0, optin = 0;
-        check_cuda(cudaGetDevice(&dev), "coarse device");
-        check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
-                   "coarse smem optin");
-        cudaFuncAttributes fa;
-        check_cuda(cudaFuncGetAttributes(&fa, kf), "coarse func attrs");
-        optin -= (int)fa.sharedSizeBytes;  // the static trace stamps
-        check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin),
-                   "coarse smem attr");
-        it = granted.emplace((const void*)kf, optin).first;
-      }
-      g = it->second;
-    }
+    const int g = smem_optin((const void*)kf);
     require(smem <= (size_t)g, "coarse: shared memory budget exceeded");
     kf<<<(unsigned)a.B, 32 * a.nw, smem, s>>>(a);
   };

@@ -4,8 +4,6 @@
 #pragma once
 
 #include <cmath>
-#include <mutex>
-#include <set>
 
 #include "fmgsr_device.cuh"
 #include "fmgsr_internal.h"
@@ -499,14 +497,8 @@ void ns2_fill_launch(const Ns2Desc<T0>& d, cudaStream_t s) {
   const size_t smem = (size_t)D2 * 6 * NT2 * sizeof(T);  // max(R, R2) rows per slot (48 / 96 KB)
   const bool om1 = d.omega == 1.0;
   auto go = [&](void (*kf)(const Ns2Args<T>)) {
-    if (smem > 48 * 1024) {
-      static std::mutex mu;
-      static std::set<const void*> granted;
-      std::lock_guard<std::mutex> lk(mu);
-      if (granted.insert((const void*)kf).second)
-        check_cuda(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                   "ns2 smem attr");
-    }
+    if (smem > 48 * 1024)
+      require(smem <= (size_t)smem_optin((const void*)kf), "ns2: shared memory budget exceeded");
     kf<<<(unsigned)blocks, NT2, smem, s>>>(a);
   };
 #define NS2_OM(SRCV, CRV, NLV, EPIV)                   \

@@ -161,12 +161,8 @@ template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool F
 static void launch_visit_k(const VisitArgs<T>& a, i64 blocks, cudaStream_t s) {
   constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
   auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC>;
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "smem attr");
-    attr = true;
-  }
+  if (smem > 48 * 1024)
+    require(smem <= (size_t)smem_optin((const void*)k), "visit: shared memory budget exceeded");
   k<<<(unsigned)blocks, VNT, smem, s>>>(a);
 }
 
