@@ -25,7 +25,7 @@ profiles() {
   prof T16 config2 "visit_kernel<fmgsr::V2<double>, .int.2, .bool.0, .bool.1, .bool.1, .bool.0, .bool.0>" 6
   prof U16 config2 "visit_kernel<double, .int.2, .bool.1, .bool.0, .bool.1, .bool.0, .bool.0>" 0
   prof U11 config2 "visit_kernel<fmgsr::V2<double>, .int.1, .bool.0, .bool.0, .bool.1, .bool.0, .bool.0>" 2
-  prof T20 config3 "ns2_kernel<double, .int.2, .bool.0, .bool.1, .bool.1, .bool.1>" 10
+  prof T20 config3 "ns2_kernel<double, .int.2, .bool.0, .bool.1, .bool.1, .bool.1>" 9
   prof U20 config3 "ns2_kernel<double, .int.2, .bool.1, .bool.1, .bool.1, .bool.0>" 0
 }
 if [ "${1:-}" = "--profiles-only" ]; then
