@@ -330,3 +330,37 @@ def test_two_column_lanes_fp32_match_scalar_lanes(fm):
     halves = torch.cat([fm.fmg_solve(cfg, f[:, :32].contiguous())[0],
                         fm.fmg_solve(cfg, f[:, 32:].contiguous())[0]], dim=1)
     assert torch.equal(whole, halves)
+
+
+def _random_configs(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        m = int(rng.integers(6, 13))
+        P = int(2 ** rng.integers(0, m - 2))
+        b = int(rng.integers(0, 10))
+        ns = int(rng.integers(1, 3))
+        n_sr = int(rng.integers(0, 3))
+        B = int(rng.choice([1, 7, 33, 64, 96, 128, 192]))
+        coarse = int(rng.choice([-1, 0, m - 1, m, m + 1]))
+        nl = bool(rng.integers(0, 4) == 0)
+        out.append((m, P, b, ns, n_sr, B, coarse, nl))
+    return out
+
+
+@pytest.mark.parametrize("m,P,b,ns,n_sr,B,coarse,nl", _random_configs(64, 2026))
+def test_random_configurations_match_oracle(fm, oracle, m, P, b, ns, n_sr, B, coarse, nl):
+    """Seeded random sweep over geometry (P, odd and even buffers), V(1,1) /
+    V(2,2), SR depth, linear / nonlinear, batch shapes (scalar lanes, two-column
+    lanes, ragged) and coarse-level placement (auto, none, on-chip cutoffs,
+    whole solve on chip): every column bit for bit against the oracle."""
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b, nonlinear=nl))
+    if nl:
+        f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=m + b))
+    else:
+        f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + b))
+    oc = oracle.make_cfg(3, m, n_sr, ns, oracle.GEOM_PATCHES, P, b, nonlin=nl)
+    want = oracle.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=8).T
+    got = fm.fmg_solve(cfg, f, coarse=coarse)[0].cpu().numpy()
+    assert np.array_equal(got, want)
