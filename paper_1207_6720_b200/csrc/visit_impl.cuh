@@ -31,7 +31,10 @@ struct VisitArgs {
   T* fun_part;     // FUNC: per-(patch, column) partial sums [P][nrg * 32]
 };
 
-constexpr int VNT = 128;  // threads per block of the visit kernel
+#ifndef FMGSR_VNT
+#define FMGSR_VNT 128
+#endif
+constexpr int VNT = FMGSR_VNT;  // threads per block of the visit kernel
 constexpr int VD = 8;     // cp.async ring depth (pairs) per lane
 
 template <typename T, int SRC, bool CR>
@@ -44,7 +47,7 @@ __host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one
 }
 
 template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC>
-__global__ void __launch_bounds__(VNT, sizeof(T) > 8 ? 2 : 4) visit_kernel(const VisitArgs<T> a) {
+__global__ void __launch_bounds__(VNT, (sizeof(T) > 8 ? 256 : 512) / VNT) visit_kernel(const VisitArgs<T> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
