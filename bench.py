@@ -361,7 +361,11 @@ def run_gpu(args, w):
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None,
-                "traffic": traffic,
+                # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+                # finest visits (committed capture, profiles/traffic.json)
+                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "traffic_unit": "bytes per launch",
+                "traffic_detail": traffic,
                 "kernel": "visit_kernel at the finest level (T_m: FMG prolongation + "
                           "patch GS + restriction/tau; U_m: FMG prolongation + Kaczmarz CR + "
                           "patch GS)",
