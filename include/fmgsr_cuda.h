@@ -134,6 +134,55 @@ int fmgsr_direct_solve_f32(const float* f, float* u, int64_t n, int64_t B, int64
 int fmgsr_direct_solve_ws_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, double* workspace, void* stream);
 int fmgsr_direct_solve_ws_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* workspace, void* stream);
 
+/* ---- Fused level visits and the f cascade -------------------
+ * The plan's level-visit kernels, one call per visit, for a caller that drives
+ * the FMG schedule itself (the reference driver cycles.py:95-222).  A visit of
+ * level n = 2^k (uniform patches: owned width W | n, W even; b-cell buffer;
+ * one forward Gauss-Seidel sweep, V(1,1)) is one pass over the fields:
+ * prologue, additive patch smoother and, for top / down, the restriction +
+ * tau epilogue.  Epilogue visits need a DEVICE workspace of
+ * fmgsr_visit_workspace_bytes(n, W, B, dtype) bytes (edge records and
+ * arrival counters; dtype 0 = f64, 1 = f32), zero-filled once before its
+ * first use: it can then serve every later epilogue visit with the same
+ * (n, W, B) -- the counters return to their start state after each visit.
+ * Outputs must not alias inputs. */
+int64_t fmgsr_visit_workspace_bytes(int64_t n, int64_t W, int64_t B, int32_t dtype);
+/* top, cycles.py:188-197 + 101-102 (the paper's fused lines 1-5): the smoother
+ * input is prolong_fmg(uH) (uH: [n/2][ld], n >= 8), no CR; then
+ * uH_out = restrict(u) and fH_out = coarse_rhs(f, u) on level k-1.  u_out may
+ * be NULL (an SR level: u is never stored); uH_out may be NULL.  W >= 4. */
+int fmgsr_visit_top_f64(const double* uH, const double* f, double* u_out, double* uH_out,
+                        double* fH_out, int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b,
+                        double omega, void* work, void* stream);
+int fmgsr_visit_top_f32(const float* uH, const float* f, float* u_out, float* uH_out,
+                        float* fH_out, int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b,
+                        double omega, void* work, void* stream);
+/* down, cycles.py:99-105: u_out = S(u), uH_out = restrict(u_out) (may be NULL),
+ * fH_out = coarse_rhs(f, u_out).  W >= 4. */
+int fmgsr_visit_down_f64(const double* u, const double* f, double* u_out, double* uH_out,
+                         double* fH_out, int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b,
+                         double omega, void* work, void* stream);
+int fmgsr_visit_down_f32(const float* u, const float* f, float* u_out, float* uH_out,
+                         float* fH_out, int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b,
+                         double omega, void* work, void* stream);
+/* up, cycles.py:109-134: sr = 0: u_out = S(u + prolong_correction(uH - restrict(u)));
+ * sr = 1 (an SR level): u_out = S(prolong_fmg(uH)) with the Kaczmarz CR step
+ * onto uH (u is not read and may be NULL). */
+int fmgsr_visit_up_f64(const double* u, const double* uH, const double* f, double* u_out,
+                       int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b, int32_t sr,
+                       double omega, void* stream);
+int fmgsr_visit_up_f32(const float* u, const float* uH, const float* f, float* u_out,
+                       int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b, int32_t sr,
+                       double omega, void* stream);
+/* f cascade, cycles.py:178-180: f_out[j] = restrict^(j+1)(f), a DEVICE
+ * [n >> (j+1)][ld] array, for j < levels; f_out is a HOST array of `levels`
+ * device pointers.  Streams f once and writes every coarser level (six per
+ * launch). */
+int fmgsr_f_cascade_f64(const double* f, int64_t n, int64_t B, int64_t ld, int32_t levels,
+                        double* const* f_out, void* stream);
+int fmgsr_f_cascade_f32(const float* f, int64_t n, int64_t B, int64_t ld, int32_t levels,
+                        float* const* f_out, void* stream);
+
 /* ---- Synthetic inputs (BASELINE.json configs; not on the solve path) ---- */
 /* f = sum_k coef[r][k-1] sin(k pi x), uex = sum_k coef sin(k pi x)/(k pi)^2;
  * coef is a DEVICE double[B][K]; uex may be NULL. */

@@ -64,6 +64,14 @@ _SIGS = {
     "fmgsr_tau_correction": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_coarse_rhs": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_fas_correct": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "fmgsr_visit_workspace_bytes": (_i64, [_i64, _i64, _i64, _i32]),
+    "fmgsr_visit_top": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _d,
+                                  _vp, _vp]),
+    "fmgsr_visit_down": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _d,
+                                   _vp, _vp]),
+    "fmgsr_visit_up": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i32, _d,
+                                 _vp]),
+    "fmgsr_f_cascade": (C.c_int, [_vp, _i64, _i64, _i64, _i32, C.POINTER(_vp), _vp]),
     "fmgsr_direct_solve": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_direct_solve_ws": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "fmgsr_fourier_rhs": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp]),
@@ -92,7 +100,8 @@ _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmg
           "fmgsr_prolong_fmg", "fmgsr_tau_correction", "fmgsr_coarse_rhs", "fmgsr_fas_correct",
           "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_fourier_rhs",
           "fmgsr_nonlinear_rhs", "fmgsr_smooth_uniform_nl", "fmgsr_coarse_rhs_nl",
-          "fmgsr_direct_solve_nl", "fmgsr_div_check"}
+          "fmgsr_direct_solve_nl", "fmgsr_div_check", "fmgsr_visit_top", "fmgsr_visit_down",
+          "fmgsr_visit_up", "fmgsr_f_cascade"}
 
 _lib = None
 _lock = threading.Lock()

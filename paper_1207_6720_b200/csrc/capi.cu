@@ -1306,6 +1306,82 @@ static void validate_desc(const fmgsr_plan_desc& d) {
   require(!d.nonlinear || ((i64)1 << d.m0) <= 64, "nonlinear: coarsest level above 64 cells");
 }
 
+// ---- fused level visits and the f cascade: helpers of the C entry points --------
+static i64 visit_edge_bytes(i64 n, i64 W, i64 B, size_t es) {
+  const i64 P = n / W, Bp = (B + 31) / 32 * 32;
+  return ((P + 1) * 10 * Bp * (i64)es + 255) / 256 * 256;
+}
+template <typename T>
+static void api_visit_epi(int src, const T* u, const T* uH, const T* f, T* u_out, T* uH_out,
+                          T* fH_out, i64 n, i64 B, i64 ld, i64 W, i64 b, double omega,
+                          void* work, cudaStream_t s, const char* what) {
+  check_field(n, B, ld, what);
+  require(W > 0 && n % W == 0, std::string(what) + ": owned width must divide n");
+  require(work != nullptr, std::string(what) + ": workspace is null");
+  require(fH_out != nullptr, std::string(what) + ": fH_out is null");
+  require(!u_out || (u_out != u && u_out != (const T*)f), std::string(what) + ": u_out aliases an input");
+  VisitDesc<T> v;
+  v.src = src;
+  v.cr = false;
+  v.epi = true;
+  v.write_u = u_out != nullptr;
+  v.n = n;
+  v.ld = ld;
+  v.B = (int)B;
+  v.W = W;
+  v.b = b;
+  v.omega = omega;
+  v.u_src = u;
+  v.uH = uH;
+  v.f = f;
+  v.u_out = u_out;
+  v.uH_out = uH_out;
+  v.fH_out = fH_out;
+  v.E = reinterpret_cast<T*>(work);
+  v.cnt = reinterpret_cast<int*>(reinterpret_cast<char*>(work) + visit_edge_bytes(n, W, B, sizeof(T)));
+  launch_visit(v, s);
+}
+template <typename T>
+static void api_visit_up(const T* u, const T* uH, const T* f, T* u_out, i64 n, i64 B, i64 ld,
+                         i64 W, i64 b, int sr, double omega, cudaStream_t s) {
+  check_field(n, B, ld, "visit_up");
+  require(W > 0 && n % W == 0, "visit_up: owned width must divide n");
+  require(u_out != nullptr && u_out != u && u_out != uH, "visit_up: u_out is null or aliases an input");
+  VisitDesc<T> v;
+  v.src = sr ? SRC_FMG : SRC_CORR;
+  v.cr = sr != 0;
+  v.n = n;
+  v.ld = ld;
+  v.B = (int)B;
+  v.W = W;
+  v.b = b;
+  v.omega = omega;
+  v.u_src = sr ? nullptr : u;
+  v.uH = uH;
+  v.f = f;
+  v.u_out = u_out;
+  launch_visit(v, s);
+}
+template <typename T>
+static void api_f_cascade(const T* f, i64 n, i64 B, i64 ld, int levels, T* const* fo,
+                          cudaStream_t s) {
+  check_field(n, B, ld, "f_cascade");
+  require(f && fo, "f_cascade: null pointer");
+  require(levels >= 1 && levels < 63 && (n >> levels) >= 1 && n % ((i64)1 << levels) == 0,
+          "f_cascade: levels out of range for n");
+  const T* src = f;
+  i64 ns = n;
+  for (int k = 0; k < levels;) {
+    CascadeDst<T> cd;
+    while (cd.levels < 6 && k < levels) {
+      require(fo[k] != nullptr, "f_cascade: null output level");
+      cd.p[cd.levels++] = fo[k++];
+    }
+    launch_cascade(src, ns, cd, ld, (int)B, s);
+    src = cd.p[cd.levels - 1];
+    ns >>= cd.levels;
+  }
+}
 }  // namespace fmgsr
 
 using namespace fmgsr;
@@ -1515,6 +1591,50 @@ int fmgsr_direct_solve_nl_f64(const double* f, double* u, int64_t n, int64_t B, 
 int fmgsr_direct_solve_nl_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, void* s) {
   return guarded([&] { check_field(n, B, ld, "direct_solve_nl"); launch_direct_solve_nl<float>(f, u, n, ld, (int)B, S(s)); });
 }
+// ---- fused level visits and the f cascade (one call per visit) --------------------
+int64_t fmgsr_visit_workspace_bytes(int64_t n, int64_t W, int64_t B, int32_t dtype) {
+  if (n <= 0 || W <= 0 || B <= 0 || n % W || (dtype != 0 && dtype != 1)) return 0;
+  return visit_edge_bytes(n, W, B, dtype == 0 ? 8 : 4) + (n / W + 1) * ((B + 31) / 32) * 4;
+}
+#define VISIT_TD(NAME, SRCV, FIRST)                                                            \
+  int NAME##_f64(const double* a0, const double* f, double* u_out, double* uH_out,             \
+                 double* fH_out, int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b,       \
+                 double omega, void* work, void* s) {                                          \
+    return guarded([&] {                                                                       \
+      api_visit_epi<double>(SRCV, SRCV == SRC_LOAD ? a0 : nullptr, SRCV == SRC_FMG ? a0 : nullptr, \
+                            f, u_out, uH_out, fH_out, n, B, ld, W, b, omega, work, S(s), #NAME); \
+    });                                                                                        \
+  }                                                                                            \
+  int NAME##_f32(const float* a0, const float* f, float* u_out, float* uH_out, float* fH_out,  \
+                 int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b, double omega,         \
+                 void* work, void* s) {                                                        \
+    return guarded([&] {                                                                       \
+      api_visit_epi<float>(SRCV, SRCV == SRC_LOAD ? a0 : nullptr, SRCV == SRC_FMG ? a0 : nullptr, \
+                           f, u_out, uH_out, fH_out, n, B, ld, W, b, omega, work, S(s), #NAME); \
+    });                                                                                        \
+  }
+VISIT_TD(fmgsr_visit_top, SRC_FMG, 0)
+VISIT_TD(fmgsr_visit_down, SRC_LOAD, 0)
+#undef VISIT_TD
+int fmgsr_visit_up_f64(const double* u, const double* uH, const double* f, double* u_out,
+                       int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b, int32_t sr,
+                       double omega, void* s) {
+  return guarded([&] { api_visit_up<double>(u, uH, f, u_out, n, B, ld, W, b, sr, omega, S(s)); });
+}
+int fmgsr_visit_up_f32(const float* u, const float* uH, const float* f, float* u_out,
+                       int64_t n, int64_t B, int64_t ld, int64_t W, int64_t b, int32_t sr,
+                       double omega, void* s) {
+  return guarded([&] { api_visit_up<float>(u, uH, f, u_out, n, B, ld, W, b, sr, omega, S(s)); });
+}
+int fmgsr_f_cascade_f64(const double* f, int64_t n, int64_t B, int64_t ld, int32_t levels,
+                        double* const* f_out, void* s) {
+  return guarded([&] { api_f_cascade<double>(f, n, B, ld, levels, f_out, S(s)); });
+}
+int fmgsr_f_cascade_f32(const float* f, int64_t n, int64_t B, int64_t ld, int32_t levels,
+                        float* const* f_out, void* s) {
+  return guarded([&] { api_f_cascade<float>(f, n, B, ld, levels, f_out, S(s)); });
+}
+
 int fmgsr_fas_correct_f64(const double* u, const double* uH, double* out, int64_t n, int64_t B, int64_t ld, void* s) {
   return guarded([&] { check_field(n, B, ld, "fas_correct"); launch_fas_correct<double>(u, uH, out, n, ld, (int)B, S(s)); });
 }

@@ -1,0 +1,118 @@
+"""The fused level visits and the f cascade as single ABI calls
+(fmgsr_visit_{top,down,up}_*, fmgsr_f_cascade_*): each returns, bit for bit,
+what the reference's operator composition returns on every column (the
+oracle restates those operators: prolong_fmg / prolong_correction, the
+additive patch smoother, restrict, coarse_rhs)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _patches(n, W, b):
+    olo = np.arange(0, n, W, dtype=np.int64)
+    ohi = olo + W
+    elo = np.maximum(olo - b, 0)
+    ehi = np.minimum(ohi + b, n)
+    return olo, ohi, elo, ehi
+
+
+def _smooth(O, u_in, f, n, W, b, uc=None):
+    k = n.bit_length() - 1
+    return O.smooth_patches(u_in, f, 4.0 ** k, *_patches(n, W, b), 1, uc=uc)
+
+
+def _batch(n, B, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(n, B, generator=g, device="cuda", dtype=torch.float64)
+
+
+CASES = [(1024, 64, 16, 4), (1024, 33, 64, 1), (512, 128, 8, 3), (2048, 64, 2048, 0), (256, 1, 4, 8)]
+
+
+@pytest.mark.parametrize("n,B,W,b", CASES)
+def test_visit_top_matches_composition(fm, oracle, n, B, W, b):
+    from paper_1207_6720_b200 import visits
+
+    if W < 4:
+        pytest.skip("epilogue needs W >= 4")
+    uH = _batch(n // 2, B, 1)
+    f = _batch(n, B, 2) * 1e3
+    u, uH2, fH = visits.visit_top(uH, f, W, b)
+    none_u, uH3, fH3 = visits.visit_top(uH, f, W, b, store_u=False)
+    assert none_u is None
+    assert torch.equal(uH2, uH3) and torch.equal(fH, fH3)
+    uHh, fh = uH.cpu().numpy(), f.cpu().numpy()
+    for r in range(B):
+        ur = _smooth(oracle, oracle.prolong_fmg(uHh[:, r]), fh[:, r], n, W, b)
+        assert np.array_equal(u[:, r].cpu().numpy(), ur)
+        assert np.array_equal(uH2[:, r].cpu().numpy(), oracle.restrict(ur))
+        assert np.array_equal(fH[:, r].cpu().numpy(), oracle.coarse_rhs(fh[:, r], ur))
+
+
+@pytest.mark.parametrize("n,B,W,b", CASES)
+def test_visit_down_matches_composition(fm, oracle, n, B, W, b):
+    from paper_1207_6720_b200 import visits
+
+    if W < 4:
+        pytest.skip("epilogue needs W >= 4")
+    u = _batch(n, B, 3)
+    f = _batch(n, B, 4) * 1e3
+    for _ in range(2):  # the workspace counters return to their start state
+        un, uH, fH = visits.visit_down(u, f, W, b)
+    uh, fh = u.cpu().numpy(), f.cpu().numpy()
+    for r in range(B):
+        ur = _smooth(oracle, uh[:, r], fh[:, r], n, W, b)
+        assert np.array_equal(un[:, r].cpu().numpy(), ur)
+        assert np.array_equal(uH[:, r].cpu().numpy(), oracle.restrict(ur))
+        assert np.array_equal(fH[:, r].cpu().numpy(), oracle.coarse_rhs(fh[:, r], ur))
+
+
+@pytest.mark.parametrize("n,B,W,b", CASES)
+@pytest.mark.parametrize("sr", [False, True])
+def test_visit_up_matches_composition(fm, oracle, n, B, W, b, sr):
+    from paper_1207_6720_b200 import visits
+
+    u = _batch(n, B, 5)
+    uH = _batch(n // 2, B, 6)
+    f = _batch(n, B, 7) * 1e3
+    got = visits.visit_up(None if sr else u, uH, f, W, b, sr=sr)
+    uh, uHh, fh = u.cpu().numpy(), uH.cpu().numpy(), f.cpu().numpy()
+    for r in range(B):
+        if sr:
+            want = _smooth(oracle, oracle.prolong_fmg(uHh[:, r]), fh[:, r], n, W, b, uc=uHh[:, r])
+        else:
+            u_in = uh[:, r] + oracle.prolong_correction(uHh[:, r] - oracle.restrict(uh[:, r]))
+            want = _smooth(oracle, u_in, fh[:, r], n, W, b)
+        assert np.array_equal(got[:, r].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,B,levels", [(4096, 64, 9), (1024, 3, 10), (256, 40, 1)])
+def test_f_cascade_matches_repeated_restriction(fm, oracle, n, B, levels):
+    from paper_1207_6720_b200 import visits
+
+    f = _batch(n, B, 8)
+    outs = visits.f_cascade(f, levels)
+    assert len(outs) == levels
+    fh = f.cpu().numpy()
+    for r in range(B):
+        x = fh[:, r]
+        for j in range(levels):
+            x = oracle.restrict(x)
+            assert np.array_equal(outs[j][:, r].cpu().numpy(), x)
+
+
+def test_visit_arguments_are_validated(fm):
+    from paper_1207_6720_b200 import visits
+
+    f = torch.zeros(64, 2, device="cuda", dtype=torch.float64)
+    with pytest.raises(ValueError):
+        visits.visit_down(f, f, 3, 1)       # odd owned width
+    with pytest.raises(ValueError):
+        visits.visit_down(f, f, 2, 1)       # epilogue needs W >= 4
+    with pytest.raises(ValueError):
+        visits.visit_top(f, f, 8, 1)        # u_coarse on the wrong level
+    with pytest.raises(ValueError):
+        visits.f_cascade(f, 7)              # more levels than the field has
