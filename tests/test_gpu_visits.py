@@ -116,3 +116,39 @@ def test_visit_arguments_are_validated(fm):
         visits.visit_top(f, f, 8, 1)        # u_coarse on the wrong level
     with pytest.raises(ValueError):
         visits.f_cascade(f, 7)              # more levels than the field has
+
+
+@pytest.mark.parametrize("n_sr", [0, 1, 2])
+def test_fmg_driver_from_fused_visits_matches_plan(fm, n_sr):
+    """The reference's FMG-FAS-SR schedule (cycles.py:137-222) driven from
+    Python with one fused-visit call per level visit reproduces the native
+    plan's solution bit for bit (P = 4 patches, b = 2: owned width >= 4 on
+    every smoothed level, so every visit is a fused one)."""
+    from paper_1207_6720_b200 import visits
+
+    m0, m, P, b, B = 3, 10, 4, 2, 64
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(m0, m), n_sr=n_sr,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=P, buffer=b))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=12))
+    want = fm.fmg_solve(cfg, f)[0]
+
+    W = {l: max(2, 2 ** l // P) for l in range(m0, m + 1)}
+    sr = {l: l > m - n_sr for l in range(m0, m + 1)}
+    f_orig = {m: f}
+    for j, fl in enumerate(visits.f_cascade(f, m - m0)):   # cycles.py:178-180
+        f_orig[m - 1 - j] = fl
+    u = {m0: fm.direct_solve(f_orig[m0])}                   # cycles.py:183
+    for t in range(m0 + 1, m + 1):                          # cycles.py:187-199
+        fw = {t: f_orig[t]}
+        ut, u[t - 1], fw[t - 1] = visits.visit_top(u[t - 1], f_orig[t], W[t], b,
+                                                   store_u=not sr[t])
+        u[t] = ut
+        for l in range(t - 1, m0, -1):                      # down leg, cycles.py:95-106
+            u[l], ul1, fw[l - 1] = visits.visit_down(u[l], fw[l], W[l], b,
+                                                     restrict_u=l - 1 > m0)
+            if ul1 is not None:
+                u[l - 1] = ul1
+        u[m0] = fm.direct_solve(fw[m0])
+        for l in range(m0 + 1, t + 1):                      # up leg, cycles.py:109-134
+            u[l] = visits.visit_up(None if sr[l] else u[l], u[l - 1], fw[l], W[l], b, sr=sr[l])
+    assert torch.equal(u[m], want)
