@@ -269,6 +269,11 @@ int fmgsr_plan_solve_host_ex(void* plan, const void* h_forcing, void* h_solution
  * patches in order, so the result is deterministic. */
 int fmgsr_plan_solve_functional(void* plan, const void* forcing, const void* weights,
                                 void* functional, void* stream);
+/* CUDA-event durations (ms) of the finest-level top and up visits of the most
+ * recent COMPLETED solve on this plan (events recorded inside the captured
+ * graph around those two kernels); -1 when the finest level ran inside the
+ * on-chip coarse kernel.  Call after the solve's stream has synchronised. */
+int fmgsr_plan_probe_ms(void* plan, float* ms_top, float* ms_up);
 /* Same solve launched op by op (no graph) with per-visit CUDA events for
  * profiling: writes up to `cap` visit durations (ms) and their levels. */
 int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void* stream,

@@ -82,6 +82,7 @@ _SIGS = {
     "fmgsr_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_vp)]),
     "fmgsr_plan_destroy": (C.c_int, [_vp]),
     "fmgsr_plan_get_info": (C.c_int, [_vp, C.POINTER(PlanInfo)]),
+    "fmgsr_plan_probe_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "fmgsr_plan_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fmgsr_plan_solve_host": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "fmgsr_plan_solve_host_ex": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),

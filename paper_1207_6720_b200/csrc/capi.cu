@@ -104,6 +104,8 @@ struct PlanBase {
   fmgsr_plan_desc d{};
   virtual ~PlanBase() {}
   virtual void solve(const void* in, void* out, cudaStream_t s) = 0;
+  // durations (ms) of the finest top / up visits of the last completed solve; -1 if none
+  virtual void probe_ms(float* top, float* up) { *top = *up = -1.0f; }
   virtual void solve_timed(const void* in, void* out, cudaStream_t s, float* ms, int32_t* lvl,
                            int32_t* kind, i64 cap, i64* nv) = 0;
   virtual void info(fmgsr_plan_info* inf) = 0;
@@ -132,6 +134,11 @@ struct Plan : PlanBase {
   i64 ws_bytes = 0;
   cudaStream_t cap = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
+  // probe events around the finest-level top and up visits, recorded by every
+  // solve (as event-record nodes inside the captured graphs): after a solve
+  // completes they hold that solve's durations of T_m and U_m
+  cudaEvent_t probe_ev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int probe_open = -1;
   // per-solve bookkeeping (filled by enqueue)
   i64 n_launch = 0, n_visit = 0;
   // timing hooks
@@ -296,6 +303,8 @@ struct Plan : PlanBase {
       if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
     }
     tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
+    for (auto& pe : probe_ev)
+      for (auto& e : pe) check_cuda(cudaEventCreate(&e), "probe event");
     if (scratch_rows) {
       sld = Bp;
       scratch = alloc((size_t)scratch_rows * sld * sizeof(T));
@@ -358,6 +367,9 @@ struct Plan : PlanBase {
 
   ~Plan() override {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& pe : probe_ev)
+      for (auto e : pe)
+        if (e) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : hev) cudaEventDestroy(e);
     if (cap) cudaStreamDestroy(cap);
@@ -430,8 +442,23 @@ struct Plan : PlanBase {
   }
 
   // ---- visit emitters ---------------------------------------------------
+  // inside a stream capture an event record becomes a graph node only with
+  // cudaEventRecordExternal (a plain record is a capture-internal dependency)
+  static void probe_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    check_cuda(cudaStreamIsCapturing(s, &st), "capture status");
+    if (st == cudaStreamCaptureStatusActive)
+      check_cuda(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal), "probe record");
+    else
+      check_cuda(cudaEventRecord(e, s), "probe record");
+  }
   void mark_begin(cudaStream_t s, int lvl, int kind) {
     n_visit++;
+    probe_open = -1;
+    if (lvl == d.m && (kind == VK_TOP || kind == VK_UP) && probe_ev[0][0]) {
+      probe_open = kind == VK_TOP ? 0 : 1;
+      probe_record(probe_ev[probe_open][0], s);
+    }
     if (!timing) return;
     cudaEvent_t a;
     check_cuda(cudaEventCreate(&a), "event");
@@ -441,6 +468,10 @@ struct Plan : PlanBase {
     ev_kind.push_back(kind);
   }
   void mark_end(cudaStream_t s) {
+    if (probe_open >= 0) {
+      probe_record(probe_ev[probe_open][1], s);
+      probe_open = -1;
+    }
     if (!timing) return;
     cudaEvent_t b;
     check_cuda(cudaEventCreate(&b), "event");
@@ -1035,6 +1066,18 @@ struct Plan : PlanBase {
       it = graphs.emplace(key, ex).first;
     }
     check_cuda(cudaGraphLaunch(it->second, s), "graph launch");
+  }
+
+  void probe_ms(float* top, float* up) override {
+    float* out[2] = {top, up};
+    for (int k = 0; k < 2; k++) {
+      *out[k] = -1.0f;
+      if (!probe_ev[k][0]) continue;
+      float ms = 0.0f;
+      // events never recorded (finest visit inside the coarse kernel) report not-ready
+      if (cudaEventElapsedTime(&ms, probe_ev[k][0], probe_ev[k][1]) == cudaSuccess) *out[k] = ms;
+      else cudaGetLastError();
+    }
   }
 
   void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) override {
@@ -1752,6 +1795,13 @@ int fmgsr_plan_get_info(void* plan, fmgsr_plan_info* info) {
   return guarded([&] {
     require(plan && info, "plan_get_info: null argument");
     reinterpret_cast<PlanBase*>(plan)->info(info);
+  });
+}
+
+int fmgsr_plan_probe_ms(void* plan, float* ms_top, float* ms_up) {
+  return guarded([&] {
+    require(plan && ms_top && ms_up, "plan_probe_ms: null argument");
+    reinterpret_cast<PlanBase*>(plan)->probe_ms(ms_top, ms_up);
   });
 }
 int fmgsr_plan_solve(void* plan, const void* forcing, void* solution, void* stream) {

@@ -154,6 +154,14 @@ class FmgPlan:
         names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade", 5: "coarse"}
         return [(names[kind[i]], lvl[i], ms[i]) for i in range(min(nv.value, cap))]
 
+    def probe_ms(self) -> tuple[float, float]:
+        """CUDA-event durations (ms) of the finest top / up visits of the last
+        completed solve -- measured inside the replayed graph (-1: the finest
+        level ran inside the on-chip coarse kernel).  Synchronise first."""
+        t, u = C.c_float(), C.c_float()
+        N.check(N.lib().fmgsr_plan_probe_ms(self._h, C.byref(t), C.byref(u)), "plan_probe_ms")
+        return t.value, u.value
+
     def info(self) -> dict:
         inf = N.PlanInfo()
         N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")

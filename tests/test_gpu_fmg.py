@@ -364,3 +364,27 @@ def test_random_configurations_match_oracle(fm, oracle, m, P, b, ns, n_sr, B, co
     want = oracle.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=8).T
     got = fm.fmg_solve(cfg, f, coarse=coarse)[0].cpu().numpy()
     assert np.array_equal(got, want)
+
+
+def test_plan_probe_events_time_the_finest_visits(fm):
+    """fmgsr_plan_probe_ms: CUDA events recorded inside the replayed graph
+    around the finest top / up visits (what bench.py's roofline divides by);
+    -1 when the whole solve runs inside the on-chip coarse kernel."""
+    m, B = 13, 64
+    cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, m), n_sr=1,
+                          smoother=fm.SmootherConfig(ns=1, n_patches=64, buffer=4))
+    f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=3))
+    plan = fm.get_plan(fm.key_from_config(cfg, B, torch.float64))
+    sol = plan.solve(f)
+    torch.cuda.synchronize()
+    t, u = plan.probe_ms()
+    assert 0 < t < 1e3 and 0 < u < 1e3
+    assert torch.equal(sol, plan.solve(f))  # the probe nodes change nothing
+    small = fm.SolverConfig(hierarchy=fm.build_hierarchy(3, 10), n_sr=1,
+                            smoother=fm.SmootherConfig(ns=1, n_patches=4, buffer=2))
+    f1, _ = fm.fourier_batch(2 ** 10, fm.fourier_coefficients(1, seed=3))
+    whole = fm.get_plan(fm.key_from_config(small, 1, torch.float64))
+    whole.solve(f1)
+    torch.cuda.synchronize()
+    if whole.info()["coarse_cutoff"] == 10:
+        assert whole.probe_ms() == (-1.0, -1.0)
