@@ -17,7 +17,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmgsr_cuda.so")
+# FMGSR_LIB: an alternative in-tree build of the library (A/B experiments)
+LIB_PATH = os.environ.get("FMGSR_LIB") or os.path.join(_HERE, "libfmgsr_cuda.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 _i64 = C.c_int64
