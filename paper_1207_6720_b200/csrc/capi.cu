@@ -255,7 +255,11 @@ struct Plan : PlanBase {
       while (cw * 2 <= 32 && cw * 2 * target <= d.B) cw *= 2;
       CW = (int)cw;
       Lc = m0;
-      while (Lc + 1 <= m - 1 && coarse_smem_bytes<T>(m0, Lc + 1, CW) <= 200 * 1024) Lc++;
+      // an on-chip SR level adds a projected-copy buffer of 2^Lc cells per column
+      auto smem_at = [&](int lc) {
+        return coarse_smem_bytes<T>(m0, lc, CW, lc > m - d.n_sr ? 1 << lc : 0);
+      };
+      while (Lc + 1 <= m - 1 && smem_at(Lc + 1) <= 200 * 1024) Lc++;
       int want = d.coarse;
       if (want < 0)
         if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
@@ -269,7 +273,7 @@ struct Plan : PlanBase {
       int dev = 0, nsm = 0;
       check_cuda(cudaGetDevice(&dev), "device");
       check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
-      const bool fits = coarse_smem_bytes<T>(m0, m, CW) <= 200 * 1024 &&
+      const bool fits = smem_at(m) <= 200 * 1024 &&
                         (d.B + CW - 1) / CW <= nsm;
       if (S == 1 && fits && ((want < 0 && allow) || want == m + 1)) {
         whole = true;
@@ -813,6 +817,7 @@ struct Plan : PlanBase {
     a.mode = mode;
     a.CW = CW;
     a.nw = CNW;
+    a.pj = (!coarse_warp && Lc > d.m - d.n_sr) ? 1 : 0;
     a.B = (int)d.B;
     a.ld = d.ld;
     for (int l = d.m0; l <= Lc; l++) {

@@ -88,9 +88,13 @@ struct CoarseArgs {
   int lgW[32] = {}, off[32] = {}, slen[32] = {};
   int fields = 0, scratch = 0;
   int nw = 1;  // warps per column (coarse_warp_kernel)
+  // CTA kernel: 1 = a shared-memory buffer of 2^Lc x CW cells holds the
+  // Kaczmarz-projected copy of an on-chip SR level's input (coarse_smem_bytes
+  // extra_cells = 2^Lc); 0 = project just in time inside the chains
+  int pj = 0;
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
-template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW);
+template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells = 0);
 // one warp per RHS column (kernels_coarse_warp.cu): ns = 1 or 2, linear or nonlinear
 template <typename T> size_t coarse_warp_layout(CoarseArgs<T>& a, bool ns2, bool nl);
 template <typename T> void launch_coarse_warp(const CoarseArgs<T>& a, bool ns2, bool nl, cudaStream_t s);

@@ -47,6 +47,7 @@ struct CoarseCtx {
   const T* dfac;  // direct-solve factor d[n0], e[n0], RN(1/d)[n0]
   const T* efac;
   const T* rfac;
+  T* pjb = nullptr;  // projected copy of an SR level's smoother input (a.pj)
   int c0;
   unsigned curmask;
   __device__ CoarseCtx(const CoarseArgs<T>& args) : a(args) {}
@@ -203,11 +204,25 @@ struct CoarseCtx {
     }
   }
 
+  // Kaczmarz projection of every pair of the level (the values the CR pass gives
+  // the pairs a patch projects, _kernels_numba.py:42-57): pj = projected u_in
+  __device__ void phase_project(T* pj, const T* uin, const T* uc, int l) {
+    const int nc = nlev(l) >> 1;
+    for (int e = threadIdx.x; e < nc * CW; e += blockDim.x) {
+      const int j = e / CW, c = e % CW;
+      T aa = uin[(2 * j) * CW + c], bb = uin[(2 * j + 1) * CW + c];
+      kaczmarz_pair(aa, bb, uc[j * CW + c], a.kz);
+      pj[(2 * j) * CW + c] = aa;
+      pj[(2 * j + 1) * CW + c] = bb;
+    }
+  }
+
   // ---- patch chains: additive ns = 1 smoother (_kernels_numba.py:60-92) -----------
   // one chain per (patch, column) over the precomputed input uin; Kaczmarz (CR)
   // per pair inside the window; domain-boundary rows peeled off the loop.
   template <bool CR>
-  __device__ void chains(int l, const T* uin, const T* f, const T* uc, T* out) {
+  __device__ void chains(int l, const T* uin, const T* f, const T* uc, T* out,
+                         const T* pj = nullptr) {
     const int n = nlev(l), W = (int)a.W[l], b = (int)a.b[l];
     const int P = n / W;
     GsCoef<T> gc;
@@ -225,9 +240,11 @@ struct CoarseCtx {
       const T* ui = uin + c;
       const T* fc = f + c;
       T* oc = out + c;
+      const T* pc = pj ? pj + c : nullptr;
       auto val = [&](int x) -> T {
         if (!CR) return ui[x * CW];
         const int j = x >> 1;
+        if (pc) return (j >= wlo && j < whi) ? pc[x * CW] : ui[x * CW];
         T v = ui[x * CW];
         if (j >= wlo && j < whi) {
           T aa = ui[(2 * j) * CW], bb = ui[(2 * j + 1) * CW];
@@ -249,13 +266,18 @@ struct CoarseCtx {
         i = 1;
       }
       const int iend = oe < n - 1 ? oe : n - 1;
+      // f of the next cell is read one iteration ahead, so its shared-memory
+      // latency overlaps the current cell's dependent fp64 chain
+      T fi = fc[i * CW];
       for (; i < iend; i++) {
         T nn = val(i + 2 < n ? i + 2 : n - 1);
-        T v = gs_int(gc, uL, cu, nx, fc[i * CW]);
+        const T fnext = fc[(i + 1) * CW];  // i + 1 <= n - 1
+        T v = gs_int(gc, uL, cu, nx, fi);
         if (i >= os) oc[i * CW] = v;
         uL = v;
         cu = nx;
         nx = nn;
+        fi = fnext;
       }
       if (oe == n) oc[(n - 1) * CW] = gs_bnd(gc, cu, uL, fc[(n - 1) * CW]);
     }
@@ -318,7 +340,11 @@ struct CoarseCtx {
     if (s) phase_fmg(U(l, c ^ 1), uH, l);
     else phase_corr(U(l, c ^ 1), U(l, c), uH, l);
     bar("U.prolong", l);
-    if (s) chains<true>(l, U(l, c ^ 1), Fl(l), uH, U(l, c));
+    if (s && pjb) {  // project every pair once instead of per cell inside the chains
+      phase_project(pjb, U(l, c ^ 1), uH, l);
+      bar("U.project", l);
+    }
+    if (s) chains<true>(l, U(l, c ^ 1), Fl(l), uH, U(l, c), pjb);
     else chains<false>(l, U(l, c ^ 1), Fl(l), nullptr, U(l, c));
     bar("U.smooth", l);
   }
@@ -353,6 +379,7 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
   x.dfac = d;
   x.efac = e;
   x.rfac = e + n0;
+  x.pjb = a.pj ? e + 2 * n0 : nullptr;
   if (a.mode == 0) {
     x.load(x.Fl(m0), a.forig[m0], n0);
     x.bar("load", m0);
@@ -411,10 +438,10 @@ __global__ void k_cascade(const T* __restrict__ src, CascadeDst<T> dst, i64 n_sr
 }  // namespace
 
 template <typename T>
-size_t coarse_smem_bytes(int m0, int Lc, int CW) {
+size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells) {
   i64 cells = 0;
   for (int l = m0; l <= Lc; l++) cells += (i64)1 << l;
-  return (size_t)(3 * cells * CW + 3 * ((i64)1 << m0)) * sizeof(T);
+  return (size_t)(3 * cells * CW + 3 * ((i64)1 << m0) + (i64)extra_cells * CW) * sizeof(T);
 }
 
 template <typename T, int CW>
@@ -428,7 +455,7 @@ static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s
 template <typename T>
 void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
   require(a.Lc >= a.m0 && a.Lc < 31, "coarse: bad cutoff");
-  size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW);
+  size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW, a.pj ? 1 << a.Lc : 0);
   require(smem <= 227 * 1024, "coarse: shared memory budget exceeded");
   switch (a.CW) {
     case 1: launch_coarse_cw<T, 1>(a, smem, s); break;
@@ -462,8 +489,8 @@ void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, i
   check_launch("cascade");
 }
 
-template size_t coarse_smem_bytes<double>(int, int, int);
-template size_t coarse_smem_bytes<float>(int, int, int);
+template size_t coarse_smem_bytes<double>(int, int, int, int);
+template size_t coarse_smem_bytes<float>(int, int, int, int);
 template void launch_coarse<double>(const CoarseArgs<double>&, cudaStream_t);
 template void launch_coarse<float>(const CoarseArgs<float>&, cudaStream_t);
 template void launch_cascade<double>(const double*, i64, const CascadeDst<double>&, i64, int, cudaStream_t);
