@@ -273,7 +273,8 @@ struct Plan : PlanBase {
       int dev = 0, nsm = 0;
       check_cuda(cudaGetDevice(&dev), "device");
       check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
-      const bool fits = smem_at(m) <= 200 * 1024 &&
+      const bool fits = coarse_smem_bytes<T>(m0, m, CW, (m > m - d.n_sr ? 1 << m : 0) +
+                                                           (1 << (m + 1)) - (1 << m0)) <= 200 * 1024 &&
                         (d.B + CW - 1) / CW <= nsm;
       if (S == 1 && fits && ((want < 0 && allow) || want == m + 1)) {
         whole = true;
@@ -818,6 +819,7 @@ struct Plan : PlanBase {
     a.CW = CW;
     a.nw = CNW;
     a.pj = (!coarse_warp && Lc > d.m - d.n_sr) ? 1 : 0;
+    a.fo = (whole && mode == 0) ? 1 : 0;
     a.B = (int)d.B;
     a.ld = d.ld;
     for (int l = d.m0; l <= Lc; l++) {
@@ -848,7 +850,7 @@ struct Plan : PlanBase {
       st.push_back({ST_LOADF, d.m, 0});
       st.push_back({ST_CASCADE_HI, d.m, 0});
     }
-    st.push_back({ST_CASCADE_LO, d.m, 0});
+    if (!whole) st.push_back({ST_CASCADE_LO, d.m, 0});  // whole: the cascade runs on chip
     st.push_back({ST_COARSE_FMG, Lc, 0});  // whole: Lc = m, the loop below is empty
     for (int t = Lc + 1; t <= d.m; t++) {
       st.push_back({ST_TOP, t, t});

@@ -92,6 +92,10 @@ struct CoarseArgs {
   // Kaczmarz-projected copy of an on-chip SR level's input (coarse_smem_bytes
   // extra_cells = 2^Lc); 0 = project just in time inside the chains
   int pj = 0;
+  // CTA kernel, whole solve on chip (Lc = m): 1 = the f cascade runs in shared
+  // memory from forig[m] (extra 2^(m+1) - 2^m0 cells per column) instead of
+  // loading each restricted level from global memory
+  int fo = 0;
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
 template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells = 0);

@@ -48,6 +48,26 @@ struct CoarseCtx {
   const T* efac;
   const T* rfac;
   T* pjb = nullptr;  // projected copy of an SR level's smoother input (a.pj)
+  T* fob = nullptr;  // on-chip f cascade (a.fo): level l at fob + CW (2^l - 2^m0)
+  __device__ __forceinline__ T* FO(int l) const { return fob + CW * ((1 << l) - (1 << a.m0)); }
+  // f cascade of cycles.py:178-180 in shared memory: the same pair averages,
+  // level by level, as k_cascade
+  __device__ void cascade_on_chip(int m) {
+    load(FO(m), a.forig[m], 1 << m);
+    bar("load", m);
+    for (int l = m - 1; l >= a.m0; l--) {
+      const T* src = FO(l + 1);
+      T* dst = FO(l);
+      for (int e = threadIdx.x; e < (1 << l) * CW; e += blockDim.x) {
+        const int j = e / CW, c = e % CW;
+        dst[e] = xmul(T(0.5), xadd(src[(2 * j) * CW + c], src[(2 * j + 1) * CW + c]));
+      }
+      bar("cascade", l);
+    }
+  }
+  __device__ void copy(T* dst, const T* src, int n) {
+    for (int e = threadIdx.x; e < n * CW; e += blockDim.x) dst[e] = src[e];
+  }
   int c0;
   unsigned curmask;
   __device__ CoarseCtx(const CoarseArgs<T>& args) : a(args) {}
@@ -380,12 +400,19 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
   x.efac = e;
   x.rfac = e + n0;
   x.pjb = a.pj ? e + 2 * n0 : nullptr;
+  x.fob = a.fo ? e + 2 * n0 + (a.pj ? (1 << Lc) * CW : 0) : nullptr;
   if (a.mode == 0) {
-    x.load(x.Fl(m0), a.forig[m0], n0);
+    if (x.fob) {
+      x.cascade_on_chip(Lc);
+      x.copy(x.Fl(m0), x.FO(m0), n0);
+    } else {
+      x.load(x.Fl(m0), a.forig[m0], n0);
+    }
     x.bar("load", m0);
     x.visit_direct();
     for (int t = m0 + 1; t <= Lc; t++) {
-      x.load(x.Fl(t), a.forig[t], 1 << t);
+      if (x.fob) x.copy(x.Fl(t), x.FO(t), 1 << t);
+      else x.load(x.Fl(t), a.forig[t], 1 << t);
       x.bar("load", t);
       x.visit_top(t);
       for (int l = t - 1; l > m0; l--) x.visit_down(l);
@@ -455,7 +482,10 @@ static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s
 template <typename T>
 void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
   require(a.Lc >= a.m0 && a.Lc < 31, "coarse: bad cutoff");
-  size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW, a.pj ? 1 << a.Lc : 0);
+  size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW,
+                                     (a.pj ? 1 << a.Lc : 0) +
+                                         (a.fo ? (1 << (a.Lc + 1)) - (1 << a.m0) : 0));
+  require(!a.fo || (a.mode == 0 && a.Lc == a.m), "coarse: on-chip cascade needs the whole solve");
   require(smem <= 227 * 1024, "coarse: shared memory budget exceeded");
   switch (a.CW) {
     case 1: launch_coarse_cw<T, 1>(a, smem, s); break;
