@@ -714,4 +714,58 @@ __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i6
   }
 }
 
+// Both boundaries of a patch in one round: the two records are written, ONE
+// fence, both counters bumped back to back by lane 0, then each boundary this
+// warp reached second is completed -- the edge_arrive protocol with one memory
+// round trip fewer per warp.  doL: the left boundary (index biL = p, this warp
+// is its side 1, fine cell sL = os); doR: the right one (biR = p + 1, side 0,
+// sR = oe).
+template <typename T, bool NL = false>
+__device__ __forceinline__ void edge_arrive2(T* E, int* cnt, i64 ldE, int nrg, int lane, int rg,
+                                             int r, bool store, T* fH, i64 ld, T inv_h2,
+                                             T inv_H2, bool doL, i64 biL,
+                                             const EdgeRec<T>& recL, i64 sL, bool doR, i64 biR,
+                                             const EdgeRec<T>& recR, i64 sR) {
+  if (!doL && !doR) return;
+  if (doL) {
+    T* mine = E + (biL * 10 + 5) * ldE + r;
+#pragma unroll
+    for (int k = 0; k < 5; k++) mine[k * ldE] = recL.v[k];
+  }
+  if (doR) {
+    T* mine = E + (biR * 10) * ldE + r;
+#pragma unroll
+    for (int k = 0; k < 5; k++) mine[k * ldE] = recR.v[k];
+  }
+  __threadfence();
+  __syncwarp();
+  int oL = 0, oR = 0;
+  if (lane == 0) {
+    if (doL) oL = atomicAdd(cnt + biL * nrg + rg, 1);
+    if (doR) oR = atomicAdd(cnt + biR * nrg + rg, 1);
+  }
+  oL = __shfl_sync(0xffffffffu, oL, 0);
+  oR = __shfl_sync(0xffffffffu, oR, 0);
+  const bool finL = doL && (oL & 1), finR = doR && (oR & 1);
+  if (!finL && !finR) return;
+  __threadfence();
+  auto finish = [&](i64 bi, i64 s) {
+    const T* base = E + bi * 10 * ldE + r;
+    T Lr[5], Rr[5];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+      Lr[k] = ldcg(base + k * ldE);
+      Rr[k] = ldcg(base + (5 + k) * ldE);
+    }
+    T fL, fR;
+    edge_finish<T, NL>(Lr, Rr, inv_h2, inv_H2, fL, fR);
+    if (store) {
+      fH[(s / 2 - 1) * ld] = fL;
+      fH[(s / 2) * ld] = fR;
+    }
+  };
+  if (finL) finish(biL, sL);
+  if (finR) finish(biR, sR);
+}
+
 }  // namespace fmgsr

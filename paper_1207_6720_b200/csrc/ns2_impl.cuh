@@ -439,12 +439,8 @@ __global__ void __launch_bounds__(NT2, sizeof(T) > 8 ? 2 : 4) ns2_kernel(const N
   if (EPI) {
     ep.finish(store);
     const i64 ldE = (i64)a.nrg * 32;
-    if (!ep.left_dom)
-      edge_arrive<T, NL>(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, ld,
-                         os, ep.ih, ep.iH);
-    if (!ep.right_dom)
-      edge_arrive<T, NL>(a.E, a.cnt, ldE, a.nrg, p + 1, 0, ep.right, lane, rg, r, store, ep.fH_out,
-                         ld, oe, ep.ih, ep.iH);
+    edge_arrive2<T, NL>(a.E, a.cnt, ldE, a.nrg, lane, rg, r, store, ep.fH_out, ld, ep.ih, ep.iH,
+                        !ep.left_dom, p, ep.left, os, !ep.right_dom, p + 1, ep.right, oe);
   }
 }
 

@@ -128,24 +128,19 @@ __global__ void __launch_bounds__(VNT, (sizeof(T) > 8 ? 256 : 512) / VNT) visit_
   EdgeRec<T> right;
   ep.finish(store, right);
   const i64 ldE = (i64)a.nrg * 32;
-  if (!ep.left_dom) {
-    if (pl == 0 && a.left_remote) {  // slab edge: the neighbour shard finishes it
+  // slab edges of a shard go to the outbox (the neighbour shard finishes them)
+  const bool remL = !ep.left_dom && pl == 0 && a.left_remote;
+  const bool remR = !ep.right_dom && pl == a.P - 1 && a.right_remote;
+  if (remL) {
 #pragma unroll
-      for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = ep.left.v[k];
-    } else {
-      edge_arrive(a.E, a.cnt, ldE, a.nrg, p, 1, ep.left, lane, rg, r, store, ep.fH_out, a.ld, os,
-                  ep.inv_h2, ep.inv_H2);
-    }
+    for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = ep.left.v[k];
   }
-  if (!ep.right_dom) {
-    if (pl == a.P - 1 && a.right_remote) {
+  if (remR) {
 #pragma unroll
-      for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
-    } else {
-      edge_arrive(a.E, a.cnt, ldE, a.nrg, p + 1, 0, right, lane, rg, r, store, ep.fH_out, a.ld, oe,
-                  ep.inv_h2, ep.inv_H2);
-    }
+    for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
   }
+  edge_arrive2(a.E, a.cnt, ldE, a.nrg, lane, rg, r, store, ep.fH_out, a.ld, ep.inv_h2, ep.inv_H2,
+               !ep.left_dom && !remL, p, ep.left, os, !ep.right_dom && !remR, p + 1, right, oe);
 }
 
 
