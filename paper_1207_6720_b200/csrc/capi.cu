@@ -253,6 +253,7 @@ struct Plan : PlanBase {
       i64 target = 128;
       if (const char* e = getenv("FMGSR_COARSE_CTAS")) target = atoll(e);
       while (cw * 2 <= 32 && cw * 2 * target <= d.B) cw *= 2;
+      if (const char* e = getenv("FMGSR_COARSE_CW")) cw = atoll(e);  // A/B experiments
       CW = (int)cw;
       Lc = m0;
       // an on-chip SR level adds a projected-copy buffer of 2^Lc cells per column
