@@ -22,6 +22,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=400)
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--fp32", action="store_true",
+                    help="fp32: two-column-lane batches (B = 64k) against the same columns "
+                         "solved in 32-column batches (scalar lanes), bitwise")
     a = ap.parse_args()
     O.build()
     rng = np.random.default_rng(a.seed)
@@ -48,10 +51,21 @@ def main():
             f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=i))
         else:
             f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=i))
-        oc = O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b, nonlin=nl)
-        want = O.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=16).T
-        got = fm.fmg_solve(cfg, f, coarse=coarse, fused=fused)[0].cpu().numpy()
-        if not np.array_equal(got, want):
+        if a.fp32:
+            import torch
+
+            B2 = 64 * max(1, B // 64)
+            f = (f if f.shape[1] >= B2 else f.repeat(1, B2 // f.shape[1] + 1))[:, :B2]
+            f = f.float().contiguous()
+            got = fm.fmg_solve(cfg, f, coarse=coarse, fused=fused)[0].cpu().numpy()
+            want = torch.cat([fm.fmg_solve(cfg, f[:, c:c + 32].contiguous(), coarse=coarse,
+                                           fused=fused)[0] for c in range(0, B2, 32)],
+                             dim=1).cpu().numpy()
+        else:
+            oc = O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b, nonlin=nl)
+            want = O.fmg_solve_batch(oc, np.ascontiguousarray(f.cpu().numpy().T), nthreads=16).T
+            got = fm.fmg_solve(cfg, f, coarse=coarse, fused=fused)[0].cpu().numpy()
+        if not np.array_equal(got, want, equal_nan=True):
             bad += 1
             cols = np.where((got != want).any(axis=0))[0]
             print(f"MISMATCH case {i}: m0={m0} m={m} P={P} b={b} ns={ns} n_sr={n_sr} B={B} "
