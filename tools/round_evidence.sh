@@ -25,6 +25,8 @@ profiles() {
   prof T16 config2 "visit_kernel<fmgsr::V2<double>, .int.2, .bool.0, .bool.1, .bool.1, .bool.0, .bool.0>" 6
   prof U16 config2 "visit_kernel<double, .int.2, .bool.1, .bool.0, .bool.1, .bool.0, .bool.0>" 0
   prof U11 config2 "visit_kernel<fmgsr::V2<double>, .int.1, .bool.0, .bool.0, .bool.1, .bool.0, .bool.0>" 2
+  # the on-chip coarse kernel, a V-segment launch (mode 1) of config 2
+  prof C9 config2 "coarse_kernel<double, .int.8>" 3
   prof T20 config3 "ns2_kernel<double, .int.2, .bool.0, .bool.1, .bool.1, .bool.1>" 9
   prof U20 config3 "ns2_kernel<double, .int.2, .bool.1, .bool.1, .bool.1, .bool.0>" 0
 }
