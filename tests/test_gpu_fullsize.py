@@ -99,3 +99,25 @@ def test_config5_fp32_full_size(fm):
           f"median {float(gap.median()):.3e}")
     assert float(gap.max()) <= 0.15
     assert float(gap.median()) <= 2e-2
+
+
+def test_config2_full_size_matches_the_reference_itself(fm):
+    """One seeded RHS of config 2 at full size (N = 2^16, 64 patches, b = 4)
+    solved by the unmodified reference (oracle/gen_golden_full.py): the GPU
+    solution's bytes hash to the reference's SHA-256, alone and as a column of
+    a 64-RHS batch (two-column lanes)."""
+    import hashlib
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "full_size.npz"))
+    m0, m, n_sr, ns, _, P, b = (int(x) for x in g["c2/params"])
+    cfg = _cfg(fm, m, P, b, ns, n_sr)
+    f = g["c2/forcing"]
+    want = bytes(g["c2/sha256"])
+    sol = fm.fmg_solve(cfg, f)[0]
+    assert np.array_equal(sol[:64], g["c2/head"])
+    assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == want
+    batch = torch.as_tensor(np.tile(f[:, None], (1, 64)), device="cuda").contiguous()
+    bsol = fm.fmg_solve(cfg, batch)[0].cpu().numpy()
+    for c in (0, 37, 63):
+        assert hashlib.sha256(np.ascontiguousarray(bsol[:, c]).tobytes()).digest() == want

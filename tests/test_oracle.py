@@ -3,6 +3,8 @@ golden vectors produced by the reference itself (oracle/gen_golden.py), the
 reference's hand-worked known answers, and scipy's LAPACK for the coarsest
 solve.  No GPU needed."""
 
+import os
+
 import numpy as np
 import pytest
 from scipy.linalg import solve_banded, solveh_banded
@@ -197,3 +199,17 @@ def test_nonlinear_reduces_to_linear_for_tiny_fields(oracle):
     a = oracle.gs_sweep(u, f, 4.0 ** 5, 0, 32, True)
     b = oracle.gs_sweep_nl(u, f, 4.0 ** 5, 0, 32, True)
     assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(a))
+
+
+def test_oracle_matches_reference_at_full_config2_size():
+    """The oracle restatement against the reference's own solve of one seeded
+    RHS of config 2 at full size (N = 2^16, 64 patches, b = 4; fixture from
+    oracle/gen_golden_full.py): SHA-256 of the solution bytes."""
+    import hashlib
+
+    from oracle import oracle as O
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "full_size.npz"))
+    m0, m, n_sr, ns, _, P, b = (int(x) for x in g["c2/params"])
+    sol = O.fmg_solve(O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b), g["c2/forcing"])
+    assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == bytes(g["c2/sha256"])
