@@ -121,3 +121,33 @@ def test_config2_full_size_matches_the_reference_itself(fm):
     bsol = fm.fmg_solve(cfg, batch)[0].cpu().numpy()
     for c in (0, 37, 63):
         assert hashlib.sha256(np.ascontiguousarray(bsol[:, c]).tobytes()).digest() == want
+
+
+def _hash_rhs(n, salt):
+    i = np.arange(n, dtype=np.uint64)
+    h = (i * np.uint64(2654435761) + np.uint64(salt)) % np.uint64(1 << 32)
+    return h.astype(np.float64) / float(1 << 32) - 0.5
+
+
+@pytest.mark.parametrize("case,B", [("h_c2", 1024), ("h_c5_P256_b4", 256), ("h_c5_P16_b1", 64),
+                                    ("h_c5_P1024_b8", 64), ("h_c4", 64)])
+def test_full_size_matches_reference_hashes(fm, case, B):
+    """BASELINE configs 2, 5 (three geometries) and 4 at full size against the
+    reference's OWN solutions (oracle/gen_golden_full.py: SHA-256 of the
+    solution bytes for a machine-independent hash forcing): the GPU solve of
+    that RHS as one column of a full-width batch reproduces the reference's
+    bytes."""
+    import hashlib
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "full_size.npz"))
+    m0, m, n_sr, ns, _, P, b, salt = (int(x) for x in g[f"{case}/params"])
+    cfg = _cfg(fm, m, P, b, ns, n_sr)
+    f = torch.as_tensor(_hash_rhs(2 ** m, salt), device="cuda")
+    batch = f[:, None].repeat(1, B).contiguous()
+    sol = fm.fmg_solve(cfg, batch)[0]
+    want = bytes(g[f"{case}/sha256"])
+    for c in sorted({0, B // 2 + 1, B - 1}):
+        col = sol[:, c].contiguous().cpu().numpy()
+        assert np.array_equal(col[:64], g[f"{case}/head"])
+        assert hashlib.sha256(col.tobytes()).digest() == want, c

@@ -213,3 +213,25 @@ def test_oracle_matches_reference_at_full_config2_size():
     m0, m, n_sr, ns, _, P, b = (int(x) for x in g["c2/params"])
     sol = O.fmg_solve(O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b), g["c2/forcing"])
     assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == bytes(g["c2/sha256"])
+
+
+def _hash_rhs(n, salt):
+    i = np.arange(n, dtype=np.uint64)
+    h = (i * np.uint64(2654435761) + np.uint64(salt)) % np.uint64(1 << 32)
+    return h.astype(np.float64) / float(1 << 32) - 0.5
+
+
+@pytest.mark.parametrize("case", ["h_c2", "h_c5_P256_b4", "h_c5_P16_b1", "h_c5_P1024_b8", "h_c4"])
+def test_oracle_matches_reference_hashes_at_full_size(case):
+    """The oracle against the reference's own solutions at the full BASELINE
+    sizes of configs 2, 5 and 4 (N up to 2^24), for the machine-independent
+    hash forcing of oracle/gen_golden_full.py: SHA-256 of the solution bytes."""
+    import hashlib
+
+    from oracle import oracle as O
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "full_size.npz"))
+    m0, m, n_sr, ns, _, P, b, salt = (int(x) for x in g[f"{case}/params"])
+    sol = O.fmg_solve(O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b), _hash_rhs(2 ** m, salt))
+    assert np.array_equal(sol[:64], g[f"{case}/head"])
+    assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == bytes(g[f"{case}/sha256"])
