@@ -60,7 +60,11 @@ def main():
     # full BASELINE sizes with the hash forcing: configs 2, 5 (three geometries) and 4
     hcases = [("h_c2", 3, 16, 1, 1, 64, 4, 1), ("h_c5_P256_b4", 3, 20, 1, 1, 256, 4, 2),
               ("h_c5_P16_b1", 3, 20, 1, 1, 16, 1, 3), ("h_c5_P1024_b8", 3, 20, 1, 1, 1024, 8, 4),
-              ("h_c4", 3, 24, 1, 1, 4096, 8, 5)]
+              ("h_c4", 3, 24, 1, 1, 4096, 8, 5),
+              # config-3 geometry with the reference's (linear) operator, V(2,2)
+              ("h_c3lin", 3, 20, 1, 2, 256, 4, 6),
+              # config 2 at other SR depths
+              ("h_c2_sr0", 3, 16, 0, 1, 64, 4, 7), ("h_c2_sr2", 3, 16, 2, 1, 64, 4, 8)]
     for name, m0, m, n_sr, ns, P, b, salt in hcases:
         smoothers._cached_patch_arrays = lambda nn, _mode, P=P, b=b: patch_rule(nn, P, b)
         try:

@@ -130,7 +130,8 @@ def _hash_rhs(n, salt):
 
 
 @pytest.mark.parametrize("case,B", [("h_c2", 1024), ("h_c5_P256_b4", 256), ("h_c5_P16_b1", 64),
-                                    ("h_c5_P1024_b8", 64), ("h_c4", 64)])
+                                    ("h_c5_P1024_b8", 64), ("h_c4", 64), ("h_c3lin", 256),
+                                    ("h_c2_sr0", 1024), ("h_c2_sr2", 1024)])
 def test_full_size_matches_reference_hashes(fm, case, B):
     """BASELINE configs 2, 5 (three geometries) and 4 at full size against the
     reference's OWN solutions (oracle/gen_golden_full.py: SHA-256 of the

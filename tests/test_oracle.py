@@ -221,7 +221,8 @@ def _hash_rhs(n, salt):
     return h.astype(np.float64) / float(1 << 32) - 0.5
 
 
-@pytest.mark.parametrize("case", ["h_c2", "h_c5_P256_b4", "h_c5_P16_b1", "h_c5_P1024_b8", "h_c4"])
+@pytest.mark.parametrize("case", ["h_c2", "h_c5_P256_b4", "h_c5_P16_b1", "h_c5_P1024_b8", "h_c4",
+                                  "h_c3lin", "h_c2_sr0", "h_c2_sr2"])
 def test_oracle_matches_reference_hashes_at_full_size(case):
     """The oracle against the reference's own solutions at the full BASELINE
     sizes of configs 2, 5 and 4 (N up to 2^24), for the machine-independent
