@@ -303,6 +303,37 @@ int fmgsr_shard_group_create(const fmgsr_plan_desc* desc, int32_t shards, void**
 int fmgsr_shard_group_solve(void* group, const void* forcing, void* solution, void* stream);
 int fmgsr_shard_group_cutoff(void* group, int32_t* cutoff, int64_t* halo_rows);
 int fmgsr_shard_group_destroy(void* group);
+/* One shard's plan with NO transport (no NCCL, no peer): the same kernels and
+ * fix-ups as fmgsr_shard_plan_create on rank `rank` of `shards`, halos never
+ * arrive.  For timing one shard's share of the work on one GPU; the result is
+ * not a solve.  Destroy with fmgsr_plan_destroy. */
+int fmgsr_shard_plan_create_local(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                                  void** plan);
+/* The communication schedule of shard `rank` of `shards`, computed on the
+ * host only (no device call; addresses are plan-relative): one record per
+ * ncclSend / ncclRecv / in-place ncclAllGather / slab-edge fix-up launch, in
+ * the order the plan issues them after each step.  Records beyond `cap` are
+ * counted in *n but not written.  *cutoff = the replication cutoff level,
+ * *halo_rows = halo rows per slab side. */
+typedef struct fmgsr_comm_rec {
+  int32_t step;        /* index in the plan's step list */
+  int32_t step_kind;   /* FMGSR_STEP_* */
+  int32_t level;       /* the step's level */
+  int32_t array_level; /* level of the array moved (-1: a tau edge record) */
+  int32_t pad;
+  int32_t kind;        /* FMGSR_COMM_* */
+  int32_t peer;      /* send / recv: the peer rank; otherwise -1 */
+  int32_t tag;       /* send / recv: pairing tag (a send meets the peer's recv of equal tag) */
+  int64_t bytes;     /* send / recv / fix-up: bytes; all-gather: bytes per rank */
+  uint64_t addr;     /* plan-relative address of the buffer (all-gather: the full array) */
+} fmgsr_comm_rec;
+enum { FMGSR_COMM_SEND = 0, FMGSR_COMM_RECV = 1, FMGSR_COMM_ALLGATHER = 2, FMGSR_COMM_FIXUP = 3 };
+enum { FMGSR_STEP_LOADF = 0, FMGSR_STEP_CASCADE_HI = 1, FMGSR_STEP_CASCADE_LO = 2,
+       FMGSR_STEP_COARSE_FMG = 3, FMGSR_STEP_TOP = 4, FMGSR_STEP_DOWN = 5,
+       FMGSR_STEP_COARSE_V = 6, FMGSR_STEP_UP = 7 };
+int fmgsr_shard_schedule(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                         fmgsr_comm_rec* recs, int64_t cap, int64_t* n, int32_t* cutoff,
+                         int64_t* halo_rows);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,21 @@ class PlanDesc(C.Structure):
     ]
 
 
+class CommRec(C.Structure):  # fmgsr_comm_rec
+    _fields_ = [
+        ("step", C.c_int32),
+        ("step_kind", C.c_int32),
+        ("level", C.c_int32),
+        ("array_level", C.c_int32),
+        ("pad", C.c_int32),
+        ("kind", C.c_int32),
+        ("peer", C.c_int32),
+        ("tag", C.c_int32),
+        ("bytes", C.c_int64),
+        ("addr", C.c_uint64),
+    ]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [
         ("workspace_bytes", _i64), ("launches_per_solve", _i64),
@@ -96,6 +111,9 @@ _SIGS = {
     "fmgsr_shard_group_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fmgsr_shard_group_cutoff": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i64)]),
     "fmgsr_shard_group_destroy": (C.c_int, [_vp]),
+    "fmgsr_shard_plan_create_local": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, C.POINTER(_vp)]),
+    "fmgsr_shard_schedule": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, _vp, _i64,
+                                       C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64)]),
 }
 _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmgsr_smooth_uniform",
           "fmgsr_apply_operator", "fmgsr_restrict", "fmgsr_prolong_correction",

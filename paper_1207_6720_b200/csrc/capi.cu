@@ -92,6 +92,7 @@ struct Xfer {
   void* ptr;
   size_t bytes;
   int tag;
+  int lvl;  // level of the array moved (-1: tau edge record)
 };
 struct Gather {
   char* base;    // the full (replicated) array
@@ -131,6 +132,7 @@ struct Plan : PlanBase {
   int* cnt_all = nullptr;
   size_t cnt_bytes = 0;
   std::vector<void*> allocs;
+  std::vector<size_t> alloc_sizes;
   i64 ws_bytes = 0;
   cudaStream_t cap = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
@@ -166,15 +168,70 @@ struct Plan : PlanBase {
 
   bool is_sr(int l) const { return l > d.m - d.n_sr; }
 
+  // Dry plans (fmgsr_shard_schedule) run the host logic only -- geometry,
+  // cutoffs, the step list and its level ping-pong state -- with every device
+  // call skipped and fake addresses, so the communication schedule can be
+  // exported and checked without a GPU.  The B200's attributes stand in for
+  // the device's.
+  bool dry = false;
+  uintptr_t dry_next = (uintptr_t)1 << 44;
+  // local shard plans (fmgsr_shard_plan_create_local): no transport at all,
+  // for timing one shard's work on one GPU (results are not a solve)
+  bool local = false;
+  int devattr(cudaDeviceAttr a, int b200) const {
+    if (dry) return b200;
+    int dev = 0, v = 0;
+    check_cuda(cudaGetDevice(&dev), "device");
+    check_cuda(cudaDeviceGetAttribute(&v, a, dev), "device attribute");
+    return v;
+  }
+#define FMGSR_PLAN_FWD(NAME) \
+  template <class... A> void NAME(A&&... a) { if (!dry) fmgsr::NAME(std::forward<A>(a)...); }
+  FMGSR_PLAN_FWD(launch_visit)
+  FMGSR_PLAN_FWD(launch_restrict_tau)
+  FMGSR_PLAN_FWD(launch_prolong_fmg)
+  FMGSR_PLAN_FWD(launch_fas_correct)
+  FMGSR_PLAN_FWD(launch_direct_solve)
+  FMGSR_PLAN_FWD(launch_direct_solve_nl)
+  FMGSR_PLAN_FWD(launch_coarse)
+  FMGSR_PLAN_FWD(launch_coarse_warp)
+  FMGSR_PLAN_FWD(launch_cascade)
+  FMGSR_PLAN_FWD(launch_smooth_ns2)
+  FMGSR_PLAN_FWD(launch_smooth_scratch)
+  FMGSR_PLAN_FWD(launch_edge_fix)
+  FMGSR_PLAN_FWD(launch_functional_field)
+  FMGSR_PLAN_FWD(launch_functional_reduce)
+#undef FMGSR_PLAN_FWD
+
   T* alloc(size_t bytes) {
+    if (dry) {
+      const uintptr_t p = dry_next;
+      dry_next += (bytes + 255) / 256 * 256 + 4096;
+      ws_bytes += (i64)bytes;
+      return (T*)p;
+    }
     void* p = nullptr;
     check_cuda(cudaMalloc(&p, bytes ? bytes : 16), "plan workspace cudaMalloc");
     allocs.push_back(p);
+    alloc_sizes.push_back(bytes ? bytes : 16);
     ws_bytes += (i64)bytes;
     return (T*)p;
   }
 
-  explicit Plan(const fmgsr_plan_desc& desc, int shards = 1, int shard = 0) {
+  // A constructor that throws never runs the destructor: release() frees
+  // whatever was created so far (also called by the destructor).
+  explicit Plan(const fmgsr_plan_desc& desc, int shards = 1, int shard = 0, bool dry_ = false,
+                bool local_ = false) {
+    dry = dry_;
+    local = local_;
+    try {
+      init(desc, shards, shard);
+    } catch (...) {
+      release();
+      throw;
+    }
+  }
+  void init(const fmgsr_plan_desc& desc, int shards, int shard) {
     d = desc;
     S = shards;
     srank = shard;
@@ -212,10 +269,8 @@ struct Plan : PlanBase {
       // deepest Lc whose per-warp slice fits and keeps all B warps in one wave
       CW = 1;
       Lc = m0;
-      int dev = 0, smsm = 0, nsm = 0;
-      check_cuda(cudaGetDevice(&dev), "device");
-      check_cuda(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem/SM");
-      check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
+      const int smsm = devattr(cudaDevAttrMaxSharedMemoryPerMultiprocessor, 233472);
+      const int nsm = devattr(cudaDevAttrMultiProcessorCount, 148);
       // warps per column: one chain per thread on the deepest level (a
       // thread's serial work grows with P_l / (32 NW)), at most 8 warps
       auto nw_for = [&](int lc) {
@@ -242,6 +297,15 @@ struct Plan : PlanBase {
         return per_sm >= 1 && per_sm * nsm >= d.B;
       };
       while (Lc + 1 <= m - 1 && fits(Lc + 1)) Lc++;
+      {  // the coarsest level itself must fit one CTA's shared memory
+        CoarseArgs<T> t;
+        t.m0 = m0;
+        t.Lc = m0;
+        t.nw = nw_for(m0);
+        t.W[m0] = lv[m0].W;
+        t.b[m0] = lv[m0].b;
+        if (coarse_warp_layout(t, d.ns == 2, d.nonlinear != 0) > 227 * 1024) use_coarse = false;
+      }
       int want = d.coarse;
       if (want < 0)
         if (const char* e = getenv("FMGSR_COARSE_LC")) want = atoi(e) + 1;
@@ -260,6 +324,9 @@ struct Plan : PlanBase {
       auto smem_at = [&](int lc) {
         return coarse_smem_bytes<T>(m0, lc, CW, lc > m - d.n_sr ? 1 << lc : 0);
       };
+      // the coarsest level itself must fit: fewer columns per CTA, else no coarse kernel
+      while (CW > 1 && smem_at(m0) > 200 * 1024) CW /= 2;
+      if (smem_at(m0) > 200 * 1024) use_coarse = false;
       while (Lc + 1 <= m - 1 && smem_at(Lc + 1) <= 200 * 1024) Lc++;
       int want = d.coarse;
       if (want < 0)
@@ -271,9 +338,7 @@ struct Plan : PlanBase {
       // launches (auto, or coarse = m + 1; FMGSR_COARSE_WHOLE=0 disables).
       const char* we = getenv("FMGSR_COARSE_WHOLE");
       const bool allow = !(we && we[0] == '0');
-      int dev = 0, nsm = 0;
-      check_cuda(cudaGetDevice(&dev), "device");
-      check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "SMs");
+      const int nsm = devattr(cudaDevAttrMultiProcessorCount, 148);
       const bool fits = coarse_smem_bytes<T>(m0, m, CW, (m > m - d.n_sr ? 1 << m : 0) +
                                                            (1 << (m + 1)) - (1 << m0)) <= 200 * 1024 &&
                         (d.B + CW - 1) / CW <= nsm;
@@ -283,6 +348,7 @@ struct Plan : PlanBase {
       }
     }
     if (S > 1) {
+      require(use_coarse, "sharding needs the on-chip coarse levels (coarse != 0)");
       plan_shards(Bp);
       finish_shards();
     }
@@ -309,15 +375,19 @@ struct Plan : PlanBase {
       if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
     }
     tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
-    for (auto& pe : probe_ev)
-      for (auto& e : pe) check_cuda(cudaEventCreate(&e), "probe event");
+    if (!dry)
+      for (auto& pe : probe_ev)
+        for (auto& e : pe) check_cuda(cudaEventCreate(&e), "probe event");
     if (scratch_rows) {
       sld = Bp;
       scratch = alloc((size_t)scratch_rows * sld * sizeof(T));
     }
     cnt_bytes = (size_t)cnt_total * sizeof(int);
     cnt_all = (int*)alloc(cnt_bytes);
-    check_cuda(cudaMemset(cnt_all, 0, cnt_bytes ? cnt_bytes : 16), "plan memset");
+    if (!dry) check_cuda(cudaMemset(cnt_all, 0, cnt_bytes ? cnt_bytes : 16), "plan memset");
+    if (local)  // no halo ever arrives: keep the never-written rows finite
+      for (size_t k = 0; k < allocs.size(); k++)
+        check_cuda(cudaMemset(allocs[k], 0, alloc_sizes[k]), "plan memset");
     i64 off = 0;
     for (int l = m0 + 1; l <= m; l++) {
       Level& L = lv[l];
@@ -326,7 +396,7 @@ struct Plan : PlanBase {
         off += (L.n / L.W + 1) * nrg;
       }
     }
-    check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
+    if (!dry) check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
   }
 
   // Replication cutoff: every level above Lr must split into S slabs of whole
@@ -371,18 +441,28 @@ struct Plan : PlanBase {
     }
   }
 
-  ~Plan() override {
+  ~Plan() override { release(); }
+  void release() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+    for (auto& kv : fgraphs) cudaGraphExecDestroy(kv.second);
+    fgraphs.clear();
     for (auto& pe : probe_ev)
-      for (auto e : pe)
-        if (e) cudaEventDestroy(e);
+      for (auto& e : pe)
+        if (e) cudaEventDestroy(e), e = nullptr;
     for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
     for (auto e : hev) cudaEventDestroy(e);
-    if (cap) cudaStreamDestroy(cap);
-    if (s_in) cudaStreamDestroy(s_in);
-    if (s_out) cudaStreamDestroy(s_out);
+    hev.clear();
+    if (cap) cudaStreamDestroy(cap), cap = nullptr;
+    if (s_in) cudaStreamDestroy(s_in), s_in = nullptr;
+    if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (ncomm && nccl && nccl->commDestroy) nccl->commDestroy(ncomm);
-    for (void* p : allocs) cudaFree(p);
+    ncomm = nullptr;
+    if (!dry)
+      for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    alloc_sizes.clear();
   }
 
   // ---- host-buffer solve: chunks of B columns pipelined over PCIe ---------------
@@ -450,7 +530,8 @@ struct Plan : PlanBase {
   // ---- visit emitters ---------------------------------------------------
   // inside a stream capture an event record becomes a graph node only with
   // cudaEventRecordExternal (a plain record is a capture-internal dependency)
-  static void probe_record(cudaEvent_t e, cudaStream_t s) {
+  void probe_record(cudaEvent_t e, cudaStream_t s) const {
+    if (dry) return;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     check_cuda(cudaStreamIsCapturing(s, &st), "capture status");
     if (st == cudaStreamCaptureStatusActive)
@@ -461,7 +542,7 @@ struct Plan : PlanBase {
   void mark_begin(cudaStream_t s, int lvl, int kind) {
     n_visit++;
     probe_open = -1;
-    if (lvl == d.m && (kind == VK_TOP || kind == VK_UP) && probe_ev[0][0]) {
+    if (lvl == d.m && (kind == VK_TOP || kind == VK_UP) && probe_ev[0][0] && !dry) {
       probe_open = kind == VK_TOP ? 0 : 1;
       probe_record(probe_ev[probe_open][0], s);
     }
@@ -883,7 +964,8 @@ struct Plan : PlanBase {
   void run_step(const Step& st, const T* forcing, T* solution, cudaStream_t s) {
     switch (st.kind) {
       case ST_LOADF:  // the caller's forcing slab into the halo'd finest buffer
-        check_cuda(cudaMemcpyAsync(fm + c0(d.m) * d.ld, forcing,
+        if (!dry)
+          check_cuda(cudaMemcpyAsync(fm + c0(d.m) * d.ld, forcing,
                                    (size_t)(c1(d.m) - c0(d.m)) * d.ld * sizeof(T),
                                    cudaMemcpyDeviceToDevice, s),
                    "forcing slab copy");
@@ -952,24 +1034,24 @@ struct Plan : PlanBase {
     const size_t bytes = (size_t)H * d.ld * sizeof(T);
     const i64 a = c0(l), b = c1(l);
     if (srank > 0) {
-      xs.push_back({srank - 1, true, X + a * d.ld, bytes, 2 * id});
-      xs.push_back({srank - 1, false, X + (a - H) * d.ld, bytes, 2 * id + 1});
+      xs.push_back({srank - 1, true, X + a * d.ld, bytes, 2 * id, l});
+      xs.push_back({srank - 1, false, X + (a - H) * d.ld, bytes, 2 * id + 1, l});
     }
     if (srank < S - 1) {
-      xs.push_back({srank + 1, true, X + (b - H) * d.ld, bytes, 2 * id + 1});
-      xs.push_back({srank + 1, false, X + b * d.ld, bytes, 2 * id});
+      xs.push_back({srank + 1, true, X + (b - H) * d.ld, bytes, 2 * id + 1, l});
+      xs.push_back({srank + 1, false, X + b * d.ld, bytes, 2 * id, l});
     }
   }
   void records(int l, std::vector<Xfer>& xs) const {
     const i64 slot = 5 * ((d.B + 31) / 32) * 32;
     const size_t bytes = (size_t)slot * sizeof(T);
     if (srank > 0) {
-      xs.push_back({srank - 1, true, ob[l], bytes, 0});
-      xs.push_back({srank - 1, false, ib[l], bytes, 1});
+      xs.push_back({srank - 1, true, ob[l], bytes, 0, -1});
+      xs.push_back({srank - 1, false, ib[l], bytes, 1, -1});
     }
     if (srank < S - 1) {
-      xs.push_back({srank + 1, true, ob[l] + slot, bytes, 1});
-      xs.push_back({srank + 1, false, ib[l] + slot, bytes, 0});
+      xs.push_back({srank + 1, true, ob[l] + slot, bytes, 1, -1});
+      xs.push_back({srank + 1, false, ib[l] + slot, bytes, 0, -1});
     }
   }
   // transfers, slab-edge fix-ups and all-gathers owed after step st
@@ -1024,6 +1106,43 @@ struct Plan : PlanBase {
       n_launch++;
     }
   }
+  // host-only export of the transport schedule (dry plans): one record per
+  // send / recv / all-gather / fix-up, in issue order, after every step
+  void schedule(std::vector<fmgsr_comm_rec>& out) {
+    reset_state(nullptr);
+    int si = 0;
+    T* fake = (T*)alloc((size_t)(lv[d.m].n / S) * d.ld * sizeof(T));
+    for (const Step& st : steps()) {
+      run_step(st, fake, fake, nullptr);
+      std::vector<Xfer> xs;
+      std::vector<Gather> gs;
+      comm_plan(st, xs, gs);
+      auto rec = [&](int kind, int peer, int tag, i64 bytes, const void* a, int al) {
+        fmgsr_comm_rec r;
+        r.step = si;
+        r.step_kind = st.kind;
+        r.level = st.l;
+        r.array_level = al;
+        r.pad = 0;
+        r.kind = kind;
+        r.peer = peer;
+        r.tag = tag;
+        r.bytes = bytes;
+        r.addr = (uint64_t)(uintptr_t)a;
+        out.push_back(r);
+      };
+      for (const Xfer& x : xs)
+        rec(x.send ? FMGSR_COMM_SEND : FMGSR_COMM_RECV, x.peer, x.tag, (i64)x.bytes, x.ptr, x.lvl);
+      if ((st.kind == ST_TOP || st.kind == ST_DOWN) && sharded(st.l)) {
+        const i64 slot = 5 * ((d.B + 31) / 32) * 32;
+        if (c0(st.l) > 0) rec(FMGSR_COMM_FIXUP, -1, 0, slot * (i64)sizeof(T), ib[st.l], st.l - 1);
+        if (c1(st.l) < lv[st.l].n)
+          rec(FMGSR_COMM_FIXUP, -1, 1, slot * (i64)sizeof(T), ib[st.l] + slot, st.l - 1);
+      }
+      for (const Gather& g : gs) rec(FMGSR_COMM_ALLGATHER, -1, 0, (i64)g.chunk, g.base, Lr);
+      si++;
+    }
+  }
   NcclApi* nccl = nullptr;
   void* ncomm = nullptr;
   void comm_nccl(const Step& st, cudaStream_t s);  // defined after NcclApi
@@ -1033,7 +1152,7 @@ struct Plan : PlanBase {
     n_visit = 0;
     for (int l = d.m0; l <= d.m; l++) lv[l].cur = 0;
     if (cnt_bytes) {
-      check_cuda(cudaMemsetAsync(cnt_all, 0, cnt_bytes, s), "counter reset");
+      if (!dry) check_cuda(cudaMemsetAsync(cnt_all, 0, cnt_bytes, s), "counter reset");
       n_launch++;
     }
   }
@@ -1238,6 +1357,10 @@ struct NcclApi {
 // then the slab-edge fix-ups, then in-place ncclAllGather of the cutoff level.
 template <typename T>
 void Plan<T>::comm_nccl(const Step& st, cudaStream_t s) {
+  if (!nccl) {  // local shard plan (timing one shard): no transport, fix-ups still run
+    fixup(st, s);
+    return;
+  }
   std::vector<Xfer> xs;
   std::vector<Gather> gs;
   comm_plan(st, xs, gs);
@@ -1294,14 +1417,23 @@ struct ShardGroup : GroupBase {
         sh[k]->run_step(st, forcing + r0 * ld, sol + r0 * ld, s);
       }
       for (int k = 0; k < S; k++) sh[k]->comm_plan(st, xs[k], gs[k]);
-      for (int k = 0; k < S; k++)  // each send lands in the peer's matching receive
-        for (const Xfer& x : xs[k]) {
-          if (!x.send) continue;
-          const Xfer* r = nullptr;
-          for (const Xfer& y : xs[x.peer])
-            if (!y.send && y.peer == k && y.tag == x.tag && y.bytes == x.bytes) r = &y;
-          require(r != nullptr, "shard group: unmatched transfer");
-          check_cuda(cudaMemcpyAsync(r->ptr, x.ptr, x.bytes, cudaMemcpyDeviceToDevice, s), "xfer");
+      // each send lands in the peer's receive exactly as NCCL pairs them: the
+      // i-th send k -> p of a group meets the i-th receive at p from k (NCCL
+      // p2p has no tags; the tags only assert that the order lines up)
+      for (int k = 0; k < S; k++)
+        for (int p = 0; p < S; p++) {
+          std::vector<const Xfer*> snd, rcv;
+          for (const Xfer& x : xs[k])
+            if (x.send && x.peer == p) snd.push_back(&x);
+          for (const Xfer& y : xs[p])
+            if (!y.send && y.peer == k) rcv.push_back(&y);
+          require(snd.size() == rcv.size(), "shard group: unmatched transfer count");
+          for (size_t i = 0; i < snd.size(); i++) {
+            require(snd[i]->tag == rcv[i]->tag && snd[i]->bytes == rcv[i]->bytes,
+                    "shard group: send / receive order differs between peers");
+            check_cuda(cudaMemcpyAsync(rcv[i]->ptr, snd[i]->ptr, snd[i]->bytes,
+                                       cudaMemcpyDeviceToDevice, s), "xfer");
+          }
         }
       for (int k = 0; k < S; k++) sh[k]->fixup(st, s);
       for (int k = 0; k < S; k++)
@@ -1476,7 +1608,7 @@ FMGSR_BOTH(fmgsr_kaczmarz_sweep, KZ_BODY)
     return guarded([&] {                                                                     \
       check_field(n, B, ld, "smooth_patches");                                               \
       require(is_pow2(n) && n >= 2, "smooth_patches: level size must be a power of two");     \
-      double want = (double)((i64)1 << (2 * level_of(n)));                                   \
+      double want = pow4(level_of(n));                                   \
       require(inv_h2 == want, "smooth_patches: inv_h2 must be 4**level");                     \
       require(u_in != u_out, "smooth_patches: u_out must not alias u_in");                    \
       require(!use_cr || uc != nullptr, "smooth_patches: use_cr needs u_coarse");             \
@@ -1744,21 +1876,57 @@ int fmgsr_shard_plan_create(const fmgsr_plan_desc* desc, int32_t shards, int32_t
     NcclApi* api = NcclApi::get();
     ncclUniqueId uid;
     std::memcpy(&uid, nccl_id, sizeof uid);
+    // The plan (every shard-feasibility check -- deterministic, so all ranks
+    // agree -- and every allocation) comes first; the collective communicator
+    // init only once this rank can run its shard.  RAII frees either on error.
+    std::unique_ptr<PlanBase> p;
+    if (desc->dtype == 0) p.reset(new Plan<double>(*desc, shards, rank));
+    else p.reset(new Plan<float>(*desc, shards, rank));
     void* comm = nullptr;
     api->check(api->commInitRank(&comm, shards, uid, rank), "ncclCommInitRank");
-    PlanBase* p;
     if (desc->dtype == 0) {
-      auto* q = new Plan<double>(*desc, shards, rank);
+      auto* q = static_cast<Plan<double>*>(p.get());
       q->nccl = api;
       q->ncomm = comm;
-      p = q;
     } else {
-      auto* q = new Plan<float>(*desc, shards, rank);
+      auto* q = static_cast<Plan<float>*>(p.get());
       q->nccl = api;
       q->ncomm = comm;
-      p = q;
     }
-    *plan = p;
+    *plan = p.release();
+  });
+}
+int fmgsr_shard_plan_create_local(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                                  void** plan) {
+  return guarded([&] {
+    require(desc && plan, "shard_plan_create_local: null argument");
+    validate_desc(*desc);
+    require(shards >= 2 && rank >= 0 && rank < shards, "shard_plan_create_local: bad rank / shards");
+    if (desc->dtype == 0) *plan = new Plan<double>(*desc, shards, rank, false, true);
+    else *plan = new Plan<float>(*desc, shards, rank, false, true);
+  });
+}
+int fmgsr_shard_schedule(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                         fmgsr_comm_rec* recs, int64_t cap, int64_t* n, int32_t* cutoff,
+                         int64_t* halo_rows) {
+  return guarded([&] {
+    require(desc && n && cutoff && halo_rows && (recs || cap == 0), "shard_schedule: null argument");
+    validate_desc(*desc);
+    require(shards >= 2 && rank >= 0 && rank < shards, "shard_schedule: bad rank / shards");
+    std::vector<fmgsr_comm_rec> out;
+    if (desc->dtype == 0) {
+      Plan<double> p(*desc, shards, rank, true);
+      p.schedule(out);
+      *cutoff = p.Lr;
+      *halo_rows = p.H;
+    } else {
+      Plan<float> p(*desc, shards, rank, true);
+      p.schedule(out);
+      *cutoff = p.Lr;
+      *halo_rows = p.H;
+    }
+    *n = (int64_t)out.size();
+    for (int64_t k = 0; k < cap && k < (int64_t)out.size(); k++) recs[k] = out[k];
   });
 }
 int fmgsr_shard_group_create(const fmgsr_plan_desc* desc, int32_t shards, void** group) {

@@ -39,10 +39,24 @@ inline void require(bool ok, const std::string& msg) {
 // returns the granted bytes (capi.cu).
 int smem_optin(const void* kf);
 
+__host__ __device__ inline double __longlong_as_double_hd(long long b) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(b);
+#else
+  double d;
+  __builtin_memcpy(&d, &b, sizeof d);
+  return d;
+#endif
+}
 __host__ __device__ inline int level_of(i64 n) {
   int k = 0;
   while (((i64)1 << (k + 1)) <= n) k++;
   return k;
+}
+// 4^k = h^-2 of level k as an exact double (2^(2k) built from its exponent
+// bits; an integer shift would overflow for k >= 32)
+__host__ __device__ inline double pow4(int k) {
+  return __longlong_as_double_hd((long long)(1023 + 2 * k) << 52);
 }
 inline bool is_pow2(i64 n) { return n >= 1 && (n & (n - 1)) == 0; }
 

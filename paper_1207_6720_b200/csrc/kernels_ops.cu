@@ -30,7 +30,7 @@ template <typename T>
 __device__ __forceinline__ T inv_h2_of(i64 n) {
   int k = 0;
   while (((i64)1 << (k + 1)) <= n) k++;
-  return (T)(double)((i64)1 << (2 * k));
+  return (T)pow4(k);
 }
 
 // stencils.py:27-36

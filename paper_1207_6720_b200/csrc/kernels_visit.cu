@@ -235,7 +235,7 @@ __global__ void k_edge_fix(const T* __restrict__ L, const T* __restrict__ R, T* 
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= B) return;
   const int lv = level_of(nf);
-  const T ih = (T)(double)((i64)1 << (2 * lv)), iH = (T)(double)((i64)1 << (2 * (lv - 1)));
+  const T ih = (T)pow4(lv), iH = (T)pow4(lv - 1);
   T Lr[5], Rr[5];
 #pragma unroll
   for (int k = 0; k < 5; k++) {

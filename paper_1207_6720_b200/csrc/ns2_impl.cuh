@@ -467,7 +467,7 @@ void ns2_fill_launch(const Ns2Desc<T0>& d, cudaStream_t s) {
   require(d.sld / C >= a.sld, "ns2: scratch stride too small");
   a.sld = d.sld / C;
   int k = level_of(d.n);
-  double ih = (double)((i64)1 << (2 * k));
+  double ih = pow4(k);
   a.gc.inv_h2 = (T)ih;
   a.gc.rdiag = (T)(1.0 / (2.0 * ih));
   a.gc.diag_b = (T)(3.0 * ih);
@@ -483,7 +483,7 @@ void ns2_fill_launch(const Ns2Desc<T0>& d, cudaStream_t s) {
   a.f = cv(d.f);
   a.u_out = mv(d.u_out);
   a.scratch = mv(d.scratch);
-  a.inv_H2 = (T)(double)((i64)1 << (2 * (k - 1)));
+  a.inv_H2 = (T)pow4(k - 1);
   a.write_u = d.write_u;
   a.uH_out = mv(d.uH_out);
   a.fH_out = mv(d.fH_out);

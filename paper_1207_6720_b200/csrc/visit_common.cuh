@@ -12,7 +12,7 @@ template <typename T>
 static GsCoef<T> make_coef(i64 n, double omega) {
   int k = level_of(n);
   GsCoef<T> g;
-  double inv_h2 = (double)((i64)1 << (2 * k));
+  double inv_h2 = pow4(k);
   g.inv_h2 = (T)inv_h2;
   g.rdiag = (T)(1.0 / (2.0 * inv_h2));  // exact power of two
   g.diag_b = (T)(3.0 * inv_h2);

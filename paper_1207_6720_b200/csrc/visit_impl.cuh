@@ -226,7 +226,7 @@ void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   a.nrg = (a.B + 31) / 32;
   a.nc = d.n / 2;
   a.gc = make_coef<TV>(d.n, d.omega);
-  a.inv_H2 = (TV)(double)((i64)1 << (2 * (level_of(d.n) - 1)));
+  a.inv_H2 = (TV)pow4(level_of(d.n) - 1);
   a.kz = make_kz<TV>(d.proj_diag);
   a.write_u = d.write_u;
   a.u_src = cv(d.u_src);

@@ -11,6 +11,7 @@ on its fast path and what ``bench.py`` times.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -74,6 +75,9 @@ class FmgPlan:
         N.check(N.lib().fmgsr_plan_create(C.byref(d), C.byref(h)), "plan_create")
         self._h = h
         self.N = 2 ** key.m
+        self.device = torch.cuda.current_device()
+        # host-side plan state (graph map, level ping-pong) is not thread-safe
+        self._lock = threading.Lock()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -91,14 +95,18 @@ class FmgPlan:
                     or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous {k.dtype} CUDA tensor of shape "
                                  f"({self.N}, {k.B})")
+            if t.device.index != self.device:
+                raise ValueError(f"{name} is on cuda:{t.device.index}, the plan on "
+                                 f"cuda:{self.device}")
 
     def solve(self, forcing: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """One FMG pass for the (2**m, B) forcing; returns the (2**m, B) solution."""
         if out is None:
             out = torch.empty_like(forcing)
         self._check_io(forcing, out)
-        N.check(N.lib().fmgsr_plan_solve(self._h, forcing.data_ptr(), out.data_ptr(),
-                                         N.stream_ptr()), "plan_solve")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_solve(self._h, forcing.data_ptr(), out.data_ptr(),
+                                             N.stream_ptr()), "plan_solve")
         return out
 
     def solve_functional(self, forcing: torch.Tensor, weights: torch.Tensor | None = None,
@@ -114,9 +122,10 @@ class FmgPlan:
             self._check_io(weights, weights)
         if not out.is_cuda or out.dtype != k.dtype or out.numel() != k.B or not out.is_contiguous():
             raise ValueError(f"functional output must be a contiguous {k.dtype} CUDA tensor of {k.B}")
-        N.check(N.lib().fmgsr_plan_solve_functional(
-            self._h, forcing.data_ptr(), weights.data_ptr() if weights is not None else None,
-            out.data_ptr(), N.stream_ptr()), "plan_solve_functional")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_solve_functional(
+                self._h, forcing.data_ptr(), weights.data_ptr() if weights is not None else None,
+                out.data_ptr(), N.stream_ptr()), "plan_solve_functional")
         return out
 
     def solve_host(self, forcing: torch.Tensor, out: torch.Tensor, chunks: int,
@@ -133,10 +142,11 @@ class FmgPlan:
                     or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous host {k.dtype} tensor of shape "
                                  f"({self.N}, {chunks * k.B})")
-        N.check(N.lib().fmgsr_plan_solve_host_ex(self._h, forcing.data_ptr(), out.data_ptr(),
-                                                 chunks * k.B, chunks, int(bool(inputs_ready)),
-                                                 N.stream_ptr()),
-                "plan_solve_host")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_solve_host_ex(self._h, forcing.data_ptr(), out.data_ptr(),
+                                                     chunks * k.B, chunks, int(bool(inputs_ready)),
+                                                     N.stream_ptr()),
+                    "plan_solve_host")
         return out
 
     def solve_timed(self, forcing: torch.Tensor, out: torch.Tensor):
@@ -148,9 +158,10 @@ class FmgPlan:
         lvl = (C.c_int32 * cap)()
         kind = (C.c_int32 * cap)()
         nv = C.c_int64()
-        N.check(N.lib().fmgsr_plan_solve_timed(self._h, forcing.data_ptr(), out.data_ptr(),
-                                               N.stream_ptr(), ms, lvl, kind, cap,
-                                               C.byref(nv)), "plan_solve_timed")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_solve_timed(self._h, forcing.data_ptr(), out.data_ptr(),
+                                                   N.stream_ptr(), ms, lvl, kind, cap,
+                                                   C.byref(nv)), "plan_solve_timed")
         names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade", 5: "coarse"}
         return [(names[kind[i]], lvl[i], ms[i]) for i in range(min(nv.value, cap))]
 
@@ -159,12 +170,14 @@ class FmgPlan:
         completed solve -- measured inside the replayed graph (-1: the finest
         level ran inside the on-chip coarse kernel).  Synchronise first."""
         t, u = C.c_float(), C.c_float()
-        N.check(N.lib().fmgsr_plan_probe_ms(self._h, C.byref(t), C.byref(u)), "plan_probe_ms")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_probe_ms(self._h, C.byref(t), C.byref(u)), "plan_probe_ms")
         return t.value, u.value
 
     def info(self) -> dict:
         inf = N.PlanInfo()
-        N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")
         return {
             "workspace_bytes": inf.workspace_bytes,
             "launches_per_solve": inf.launches_per_solve,
@@ -176,13 +189,21 @@ class FmgPlan:
         }
 
 
-_cache: dict[PlanKey, FmgPlan] = {}
+_cache: dict[tuple, FmgPlan] = {}
+_cache_lock = threading.Lock()
 
 
 def get_plan(key: PlanKey) -> FmgPlan:
-    p = _cache.get(key)
-    if p is None:
-        if len(_cache) >= 8:
-            _cache.pop(next(iter(_cache)))
-        p = _cache[key] = FmgPlan(key)
-    return p
+    """The cached plan for ``key`` on the current device and stream.  A plan's
+    workspace, capture stream and graphs belong to the device that was current
+    when it was built, and its per-solve state (level ping-pong, edge counters)
+    is mutated by every solve, so plans are cached per (device, stream):
+    solves queued on one stream are ordered, two streams never share a plan."""
+    ck = (key, torch.cuda.current_device(), N.stream_ptr())
+    with _cache_lock:
+        p = _cache.get(ck)
+        if p is None:
+            if len(_cache) >= 8:
+                _cache.pop(next(iter(_cache)))
+            p = _cache[ck] = FmgPlan(key)
+        return p

@@ -122,6 +122,64 @@ class ShardedPlan:
     def solve(self, forcing_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = torch.empty_like(forcing_slab)
+        k = self.key
+        for name, t in (("forcing slab", forcing_slab), ("solution slab", out)):
+            if not t.is_cuda or t.dtype != k.dtype or tuple(t.shape) != (self.rows, k.B) \
+                    or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {k.dtype} CUDA tensor of shape "
+                                 f"({self.rows}, {k.B})")
+        if forcing_slab.data_ptr() == out.data_ptr():
+            raise ValueError("the solution slab must not alias the forcing slab")
         N.check(N.lib().fmgsr_plan_solve(self._h, forcing_slab.data_ptr(), out.data_ptr(),
                                          N.stream_ptr()), "plan_solve")
         return out
+
+    def info(self) -> dict:
+        inf = N.PlanInfo()
+        N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")
+        return {"workspace_bytes": inf.workspace_bytes,
+                "launches_per_solve": inf.launches_per_solve,
+                "alg_bytes_per_solve": inf.alg_bytes_per_solve}
+
+
+class LocalShardPlan(ShardedPlan):
+    """Shard ``rank`` of ``shards`` with NO transport (fmgsr_shard_plan_create_local):
+    the shard's kernels and slab-edge fix-ups on this GPU, halos never
+    exchanged.  Times one shard's share of a sharded solve on one GPU; the
+    output is not a solution."""
+
+    def __init__(self, cfg, B: int, shards: int, rank: int, dtype=torch.float64,
+                 coarse: int = -1, use_graph: bool = True):
+        N.require_cuda()
+        self.key = key_from_config(cfg, B, dtype, use_graph=use_graph, coarse=coarse)
+        d = _desc(self.key)
+        h = C.c_void_p()
+        N.check(N.lib().fmgsr_shard_plan_create_local(C.byref(d), int(shards), int(rank),
+                                                      C.byref(h)), "shard_plan_create_local")
+        self._h = h
+        self.shards, self.rank = shards, rank
+        self.rows = 2 ** self.key.m // shards
+
+
+STEP_KINDS = ("loadf", "cascade_hi", "cascade_lo", "coarse_fmg", "top", "down", "coarse_v", "up")
+COMM_KINDS = ("send", "recv", "allgather", "fixup")
+
+
+def comm_schedule(cfg, B: int, shards: int, rank: int, dtype=torch.float64, coarse: int = -1):
+    """The transport schedule of shard ``rank`` (fmgsr_shard_schedule; host
+    only, no GPU needed): ``(records, cutoff, halo_rows)`` with one dict per
+    send / recv / all-gather / fix-up in the order the plan issues them."""
+    key = key_from_config(cfg, B, dtype, coarse=coarse)
+    d = _desc(key)
+    n, cut, halo = C.c_int64(), C.c_int32(), C.c_int64()
+    L = N.lib()
+    N.check(L.fmgsr_shard_schedule(C.byref(d), int(shards), int(rank), None, 0, C.byref(n),
+                                   C.byref(cut), C.byref(halo)), "shard_schedule")
+    recs = (N.CommRec * max(1, n.value))()
+    N.check(L.fmgsr_shard_schedule(C.byref(d), int(shards), int(rank), recs, n.value,
+                                   C.byref(n), C.byref(cut), C.byref(halo)), "shard_schedule")
+    out = [{"step": r.step, "step_kind": STEP_KINDS[r.step_kind], "level": r.level,
+            "array_level": r.array_level,
+            "kind": COMM_KINDS[r.kind], "peer": r.peer, "tag": r.tag, "bytes": r.bytes,
+            "addr": r.addr} for r in recs[:n.value]]
+    return out, cut.value, halo.value

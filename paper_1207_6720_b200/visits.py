@@ -28,8 +28,11 @@ _work: dict = {}
 
 def _workspace(n: int, W: int, B: int, dt: torch.dtype, dev) -> torch.Tensor:
     """Zero-filled edge-record / counter workspace, one per (n, W, B, dtype,
-    device): the counters return to their start state after every visit."""
-    key = (n, W, B, dt, dev)
+    device, stream): the counters return to their start state after every
+    visit, so visits queued on one stream may share it; two visits running at
+    the same time on different streams must not (their arrivals would mix on
+    the same counters), hence the stream in the key."""
+    key = (n, W, B, dt, dev, N.stream_ptr())
     w = _work.get(key)
     if w is None:
         nbytes = N.lib().fmgsr_visit_workspace_bytes(n, W, B, 0 if dt == torch.float64 else 1)

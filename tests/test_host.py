@@ -112,7 +112,7 @@ def test_bench_throughput_and_config():
     import bench
 
     assert bench.throughput(2, 1024, 65536, 4.0) == pytest.approx(2 * 1024 * 65536 / 4e-3)
-    cfg = bench.workload_config("config2", bench.WORKLOADS["config2"], 8)
+    cfg = bench.workload_config("config2", bench.WORKLOADS["config2"], 8, "rhs")
     assert cfg["global_batch"] == 8 * 1024 and cfg["N"] == 2 ** 16
     assert "L2" in cfg["l2"] or "inputs larger" in cfg["l2"]
 
@@ -152,3 +152,61 @@ def test_multirank_aggregation_gloo():
     assert [r[1] for r in res] == [4.0, 4.0]
     assert res[0][2] != res[1][2]
     assert res[0][3] == pytest.approx(2 * 1024 * 2 ** 16 / 4e-3)
+
+
+# ---- multi-GPU host plumbing of bench.py (gloo, CPU) ---------------------------------------------
+def test_bench_gpus_is_authoritative():
+    import bench
+
+    bench.check_world(4, 4)
+    with pytest.raises(SystemExit, match="--gpus 8 but WORLD_SIZE=1"):
+        bench.check_world(8, 1)
+    cmd = bench.spawn_cmd(8, ["--gpus", "8", "--steps", "3"], 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "8", "--steps", "3"]
+    a = bench.parse_args(["--gpus", "2"])
+    assert a.workload == "config4" and a.shard == "patches" and a.warmup >= 3
+
+
+def test_bench_sharded_config_line():
+    import bench
+
+    c = bench.workload_config("config4", bench.WORKLOADS["config4"], 8, "patches")
+    assert c["global_batch"] == 64 and "patch slabs x8" in c["parallelism"]
+    c1 = bench.workload_config("config4", bench.WORKLOADS["config4"], 8, "rhs")
+    assert c1["global_batch"] == 8 * 64 and c1["parallelism"].startswith("dp8")
+
+
+def _shard_rank_main(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_1207_6720_b200.shard import slab
+
+    uid = bytes(range(128)) if rank == 0 else None  # stands in for ncclGetUniqueId
+    got = bench.broadcast_uid(uid, rank, device="cpu")
+    n = 2 ** 24
+    q.put((rank, got, slab(n, world, rank)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_host_side_gloo(world):
+    """run_gpu_sharded's host side: rank 0's NCCL id reaches every rank, and the
+    slabs tile the finest level exactly once."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + (os.getpid() % 500) + world
+    procs = [ctx.Process(target=_shard_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == bytes(range(128)) for r in res)
+    spans = [r[2] for r in res]
+    assert spans[0][0] == 0 and spans[-1][1] == 2 ** 24
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
