@@ -58,6 +58,8 @@ __host__ __device__ inline int level_of(i64 n) {
 __host__ __device__ inline double pow4(int k) {
   return __longlong_as_double_hd((long long)(1023 + 2 * k) << 52);
 }
+// launch shapes of the visit kernel (visit_impl.cuh VisitShape)
+enum { SHAPE_WIDE = 0, SHAPE_NARROW = 1 };
 inline bool is_pow2(i64 n) { return n >= 1 && (n & (n - 1)) == 0; }
 
 // Run f(); map exceptions to C return codes.

@@ -32,7 +32,7 @@ static bool visit_cpl2_enabled() {
 
 // the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
 // compiled in parallel)
-template <typename TV, typename T>
+template <typename TV, typename T, int SHAPE>
 void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s);
 
 // Two columns per lane: whole 64-column row groups, 2-element-aligned rows
@@ -82,8 +82,12 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
-  if (visit_cpl2_ok(d)) visit_fill_launch<V2<T>>(d, s);
-  else visit_fill_launch<T>(d, s);
+  // one launch shape (128-thread CTAs, 8-pair ring): one-warp CTAs with a
+  // 16-pair ring (VisitShape NARROW) measured slower on every few-chain case
+  // tried (config-5 P = 16: 63.1 vs 44.2 ms per cycle; an 8-way shard of
+  // config 4: 9.37 vs 8.76 ms) -- DESIGN.md 6c
+  if (visit_cpl2_ok(d)) visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
+  else visit_fill_launch<T, T, SHAPE_WIDE>(d, s);
   check_launch("visit_kernel");
 }
 

@@ -2,5 +2,5 @@
 #include "visit_impl.cuh"
 
 namespace fmgsr {
-template void visit_fill_launch<double, double>(const VisitDesc<double>&, cudaStream_t);
+template void visit_fill_launch<double, double, SHAPE_WIDE>(const VisitDesc<double>&, cudaStream_t);
 }  // namespace fmgsr

@@ -2,5 +2,5 @@
 #include "visit_impl.cuh"
 
 namespace fmgsr {
-template void visit_fill_launch<float, float>(const VisitDesc<float>&, cudaStream_t);
+template void visit_fill_launch<float, float, SHAPE_WIDE>(const VisitDesc<float>&, cudaStream_t);
 }  // namespace fmgsr

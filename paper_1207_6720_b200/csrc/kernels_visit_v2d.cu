@@ -2,5 +2,5 @@
 #include "visit_impl.cuh"
 
 namespace fmgsr {
-template void visit_fill_launch<V2<double>, double>(const VisitDesc<double>&, cudaStream_t);
+template void visit_fill_launch<V2<double>, double, SHAPE_WIDE>(const VisitDesc<double>&, cudaStream_t);
 }  // namespace fmgsr

@@ -31,23 +31,29 @@ struct VisitArgs {
   T* fun_part;     // FUNC: per-(patch, column) partial sums [P][nrg * 32]
 };
 
-#ifndef FMGSR_VNT
-#define FMGSR_VNT 128
-#endif
-constexpr int VNT = FMGSR_VNT;  // threads per block of the visit kernel
-constexpr int VD = 8;     // cp.async ring depth (pairs) per lane
+// Launch shapes of the visit kernel (threads per CTA, cp.async ring depth in
+// pairs per lane).  WIDE: 128-thread CTAs, 8-pair ring -- many chains per SM
+// (the large levels at B >= 64).  NARROW: one-warp CTAs, 16-pair ring -- few
+// chains per SM (small P x B: config-5 P = 16, one shard's slab of an S-way
+// split): the warps spread over every SM instead of leaving SMs idle behind
+// 4-warp CTAs, and each lane keeps twice the bytes in flight.
+template <int SHAPE>
+struct VisitShape {
+  static constexpr int NT = SHAPE == SHAPE_WIDE ? 128 : 32;
+  static constexpr int D = SHAPE == SHAPE_WIDE ? 8 : 16;
+};
 
-template <typename T, int SRC, bool CR>
+template <typename T, int SRC, bool CR, int NT, int D>
 __host__ __device__ constexpr size_t visit_ring_bytes() {
-  return (size_t)VD * SrcRows<SRC, CR>::R * VNT * sizeof(T);
+  return (size_t)D * SrcRows<SRC, CR>::R * NT * sizeof(T);
 }
-template <typename T, int SRC, bool CR>
+template <typename T, int SRC, bool CR, int NT, int D>
 __host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one mbarrier per (warp, slot)
-  return visit_ring_bytes<T, SRC, CR>() + (size_t)(VNT / 32) * VD * 8;
+  return visit_ring_bytes<T, SRC, CR, NT, D>() + (size_t)(NT / 32) * D * 8;
 }
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC>
-__global__ void __launch_bounds__(VNT, (sizeof(T) > 8 ? 256 : 512) / VNT) visit_kernel(const VisitArgs<T> a) {
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC, int NT, int D>
+__global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_kernel(const VisitArgs<T> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -72,13 +78,13 @@ __global__ void __launch_bounds__(VNT, (sizeof(T) > 8 ? 256 : 512) / VNT) visit_
     we = oe + a.b < a.n ? oe + a.b : a.n;
   }
 
-  Chain<T, SRC, CR, EPI, OMEGA1, VNT, VD, BULK, FUNC> ch;
+  Chain<T, SRC, CR, EPI, OMEGA1, NT, D, BULK, FUNC> ch;
   ch.lane = lane;
-  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR>()) +
-            (threadIdx.x >> 5) * VD;
+  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR, NT, D>()) +
+            (threadIdx.x >> 5) * D;
   if (BULK) {
     if (lane == 0)
-      for (int k = 0; k < VD; k++) mbar_init(ch.bars + k, 1);
+      for (int k = 0; k < D; k++) mbar_init(ch.bars + k, 1);
     mbar_fence_init();
     __syncwarp();
   }
@@ -155,13 +161,17 @@ static bool visit_bulk_enabled() {
 }
 
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC = false>
-static void launch_visit_k(const VisitArgs<T>& a, i64 blocks, cudaStream_t s) {
-  constexpr size_t smem = visit_smem_bytes<T, SRC, CR>();
-  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC>;
+template <typename T, int SHAPE, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK,
+          bool FUNC = false>
+static void launch_visit_k(const VisitArgs<T>& a, cudaStream_t s) {
+  constexpr int NT = VisitShape<SHAPE>::NT, D = VisitShape<SHAPE>::D;
+  constexpr size_t smem = visit_smem_bytes<T, SRC, CR, NT, D>();
+  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC, NT, D>;
   if (smem > 48 * 1024)
     require(smem <= (size_t)smem_optin((const void*)k), "visit: shared memory budget exceeded");
-  k<<<(unsigned)blocks, VNT, smem, s>>>(a);
+  const i64 warps = a.P * a.nrg;
+  const i64 blocks = (warps + NT / 32 - 1) / (NT / 32);
+  k<<<(unsigned)blocks, NT, smem, s>>>(a);
 }
 
 // Bulk (TMA) staging needs whole 32-column row segments at 16-byte alignment.
@@ -173,10 +183,8 @@ static bool bulk_ok(const VisitArgs<T>& a) {
          visit_bulk_enabled();
 }
 
-template <typename T, int SRC, bool CR, bool EPI>
+template <typename T, int SHAPE, int SRC, bool CR, bool EPI>
 static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
-  i64 warps = a.P * a.nrg;
-  i64 blocks = (warps + VNT / 32 - 1) / (VNT / 32);
   const bool om1 = a.gc.omega == T(1);
   // bulk (TMA) staging pays off where per-lane LDGSTS saturates the MIO
   // queue: sources with >= 5 staged rows per pair (the FAS-correction visits);
@@ -193,28 +201,28 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
     if (a.fun_part) {
       if (om1) {
-        if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true, true>(a, blocks, s);
-        else launch_visit_k<T, SRC, CR, EPI, true, false, true>(a, blocks, s);
+        if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, true, true, true>(a, s);
+        else launch_visit_k<T, SHAPE, SRC, CR, EPI, true, false, true>(a, s);
       } else {
-        if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true, true>(a, blocks, s);
-        else launch_visit_k<T, SRC, CR, EPI, false, false, true>(a, blocks, s);
+        if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, false, true, true>(a, s);
+        else launch_visit_k<T, SHAPE, SRC, CR, EPI, false, false, true>(a, s);
       }
       return;
     }
   }
   if (om1) {
-    if (bulk) launch_visit_k<T, SRC, CR, EPI, true, true>(a, blocks, s);
-    else launch_visit_k<T, SRC, CR, EPI, true, false>(a, blocks, s);
+    if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, true, true>(a, s);
+    else launch_visit_k<T, SHAPE, SRC, CR, EPI, true, false>(a, s);
   } else {
-    if (bulk) launch_visit_k<T, SRC, CR, EPI, false, true>(a, blocks, s);
-    else launch_visit_k<T, SRC, CR, EPI, false, false>(a, blocks, s);
+    if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, false, true>(a, s);
+    else launch_visit_k<T, SHAPE, SRC, CR, EPI, false, false>(a, s);
   }
 }
 
 
 // Fill the kernel arguments for lane type TV (T, or V2<T>: two columns per
 // lane) from a validated descriptor and launch.
-template <typename TV, typename T>
+template <typename TV, typename T, int SHAPE>
 void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   constexpr int C = LaneCols<TV>::value;
   auto cv = [](const T* p) { return reinterpret_cast<const TV*>(p); };
@@ -266,11 +274,11 @@ void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   if (a.P == 0) return;
 #define FMGSR_DISPATCH(SRCV)                                                    \
   if (d.cr) {                                                                  \
-    if (d.epi) launch_visit_t<TV, SRCV, true, true>(a, s);                     \
-    else launch_visit_t<TV, SRCV, true, false>(a, s);                          \
+    if (d.epi) launch_visit_t<TV, SHAPE, SRCV, true, true>(a, s);                     \
+    else launch_visit_t<TV, SHAPE, SRCV, true, false>(a, s);                          \
   } else {                                                                     \
-    if (d.epi) launch_visit_t<TV, SRCV, false, true>(a, s);                    \
-    else launch_visit_t<TV, SRCV, false, false>(a, s);                         \
+    if (d.epi) launch_visit_t<TV, SHAPE, SRCV, false, true>(a, s);                    \
+    else launch_visit_t<TV, SHAPE, SRCV, false, false>(a, s);                         \
   }
   if (d.src == SRC_LOAD) {
     FMGSR_DISPATCH(SRC_LOAD)

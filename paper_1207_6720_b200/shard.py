@@ -134,6 +134,19 @@ class ShardedPlan:
                                          N.stream_ptr()), "plan_solve")
         return out
 
+    def solve_timed(self, forcing_slab: torch.Tensor, out: torch.Tensor):
+        """Op by op with CUDA events per level visit: [(kind, level, ms)]."""
+        cap = 8192
+        ms = (C.c_float * cap)()
+        lvl = (C.c_int32 * cap)()
+        kind = (C.c_int32 * cap)()
+        nv = C.c_int64()
+        N.check(N.lib().fmgsr_plan_solve_timed(self._h, forcing_slab.data_ptr(), out.data_ptr(),
+                                               N.stream_ptr(), ms, lvl, kind, cap,
+                                               C.byref(nv)), "plan_solve_timed")
+        names = {0: "top", 1: "down", 2: "up", 3: "direct", 4: "cascade", 5: "coarse"}
+        return [(names[kind[i]], lvl[i], ms[i]) for i in range(min(nv.value, cap))]
+
     def info(self) -> dict:
         inf = N.PlanInfo()
         N.check(N.lib().fmgsr_plan_get_info(self._h, C.byref(inf)), "plan_get_info")

@@ -388,3 +388,4 @@ def test_plan_probe_events_time_the_finest_visits(fm):
     torch.cuda.synchronize()
     if whole.info()["coarse_cutoff"] == 10:
         assert whole.probe_ms() == (-1.0, -1.0)
+
