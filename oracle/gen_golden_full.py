@@ -32,7 +32,9 @@ def hash_rhs(n, salt):
     return h.astype(np.float64) / float(1 << 32) - 0.5
 
 
-def main():
+def main(only=()):
+    """Solve every case (or only the named hash cases, merged into the existing
+    fixture file)."""
     _import_reference()
     from fmgsr import cycles, smoothers
     from fmgsr.mesh import HaloMode, build_hierarchy
@@ -40,6 +42,10 @@ def main():
     orig = smoothers._cached_patch_arrays
     g = {}
     cases = [("c2", 3, 16, 1, 1, 64, 4, 0)]
+    if only:
+        old = np.load(OUT)
+        g.update({k: old[k] for k in old.files})
+        cases = []
     for name, m0, m, n_sr, ns, P, b, seed in cases:
         smoothers._cached_patch_arrays = lambda nn, _mode, P=P, b=b: patch_rule(nn, P, b)
         try:
@@ -64,8 +70,12 @@ def main():
               # config-3 geometry with the reference's (linear) operator, V(2,2)
               ("h_c3lin", 3, 20, 1, 2, 256, 4, 6),
               # config 2 at other SR depths
-              ("h_c2_sr0", 3, 16, 0, 1, 64, 4, 7), ("h_c2_sr2", 3, 16, 2, 1, 64, 4, 8)]
+              ("h_c2_sr0", 3, 16, 0, 1, 64, 4, 7), ("h_c2_sr2", 3, 16, 2, 1, 64, 4, 8),
+              # two more config-5 cells (round 2)
+              ("h_c5_P64_b1", 3, 20, 1, 1, 64, 1, 9), ("h_c5_P16_b8", 3, 20, 1, 1, 16, 8, 10)]
     for name, m0, m, n_sr, ns, P, b, salt in hcases:
+        if only and name not in only:
+            continue
         smoothers._cached_patch_arrays = lambda nn, _mode, P=P, b=b: patch_rule(nn, P, b)
         try:
             cfg = cycles.SolverConfig(hierarchy=build_hierarchy(m0, m), n_sr=n_sr,
@@ -86,4 +96,6 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    main(tuple(sys.argv[1:]))

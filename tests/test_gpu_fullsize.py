@@ -62,7 +62,10 @@ def test_config4_full_size(fm, oracle):
     assert bool((err <= 2.0 * derr).all())
 
 
-@pytest.mark.parametrize("P,b", [(16, 1), (64, 2), (256, 4), (1024, 8), (1024, 1), (16, 8)])
+CONFIG5_CELLS = [(P, b) for P in (16, 64, 256, 1024) for b in (1, 2, 4, 8)]
+
+
+@pytest.mark.parametrize("P,b", CONFIG5_CELLS)
 def test_config5_full_size_geometry(fm, oracle, P, b):
     """Config 5 geometry sweep at N = 2^20, B = 256 (fp64): oracle bit for bit
     on 2 columns, O(h^2) criterion on all, and the batch split in two halves
@@ -81,21 +84,22 @@ def test_config5_full_size_geometry(fm, oracle, P, b):
     assert torch.equal(half, sol[:, 128:])
 
 
-def test_config5_fp32_full_size(fm):
-    """Config 5 in fp32 (N = 2^20, B = 256, P = 256, b = 4) against the fp64
+@pytest.mark.parametrize("P,b", CONFIG5_CELLS)
+def test_config5_fp32_full_size(fm, P, b):
+    """Config 5 in fp32 (N = 2^20, B = 256, every (P, b) cell) against the fp64
     solve of the same forcing, at the stated tolerance: pure
     binary32 arithmetic loses ~ N * eps_32 through the h^-2 stencils (the gap
     doubles per level: measured max 1.1e-4 / 1.6e-3 / 2.8e-2 at N = 2^12 /
-    2^16 / 2^20 on 64 RHS; 5.0e-2 / median 7.8e-3 on these 256), so the bound
-    at N = 2^20 is max <= 0.15 and
+    2^16 / 2^20 on 64 RHS; 5.0e-2 / median 7.8e-3 on 256 at P = 256, b = 4),
+    so the bound at N = 2^20 is max <= 0.15 and
     median <= 2e-2 per-RHS inf-relative gap."""
-    m, P, b, B = 20, 256, 4, 256
+    m, B = 20, 256
     cfg = _cfg(fm, m, P, b, 1)
     f, uex = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=11))
     s64 = fm.fmg_solve(cfg, f)[0]
     s32 = fm.fmg_solve(cfg, f.float())[0]
     gap = (s32.double() - s64).abs().amax(0) / s64.abs().amax(0)
-    print(f"fp32 vs fp64 inf-relative gap at N=2^20: max {float(gap.max()):.3e} "
+    print(f"fp32 vs fp64 inf-relative gap at N=2^20 (P={P}, b={b}): max {float(gap.max()):.3e} "
           f"median {float(gap.median()):.3e}")
     assert float(gap.max()) <= 0.15
     assert float(gap.median()) <= 2e-2
@@ -131,7 +135,8 @@ def _hash_rhs(n, salt):
 
 @pytest.mark.parametrize("case,B", [("h_c2", 1024), ("h_c5_P256_b4", 256), ("h_c5_P16_b1", 64),
                                     ("h_c5_P1024_b8", 64), ("h_c4", 64), ("h_c3lin", 256),
-                                    ("h_c2_sr0", 1024), ("h_c2_sr2", 1024)])
+                                    ("h_c2_sr0", 1024), ("h_c2_sr2", 1024),
+                                    ("h_c5_P64_b1", 256), ("h_c5_P16_b8", 256)])
 def test_full_size_matches_reference_hashes(fm, case, B):
     """BASELINE configs 2, 5 (three geometries) and 4 at full size against the
     reference's OWN solutions (oracle/gen_golden_full.py: SHA-256 of the

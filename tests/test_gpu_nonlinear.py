@@ -125,3 +125,57 @@ def test_ns2_two_column_lanes_match_oracle(fm, oracle, nonlinear):
     for kw in (dict(), dict(coarse=0)):
         got = fm.fmg_solve(cfg, f, **kw)[0].cpu().numpy()
         assert np.array_equal(got, want), kw
+
+
+# ---- pinned to the reference's own driver (oracle/gen_golden_nl.py) ---------------------------
+def _nl_golden():
+    import os
+
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "nonlinear.npz"))
+
+
+def test_nonlinear_matches_reference_driver(fm):
+    """Every reduced-size case of tests/golden/nonlinear.npz (the reference's
+    FMG driver with the Newton-GS lane, N(u) tau and Newton coarse solve
+    injected), solved as columns of one batch (column 0 the case, the rest
+    scaled copies): the case column bit for bit, through the fused plan and the
+    operator path."""
+    g = _nl_golden()
+    for name in g["cases"]:
+        m0, m, n_sr, ns, _, P, b = (int(x) for x in g[f"{name}/params"])
+        cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(m0, m), n_sr=n_sr,
+                              smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b,
+                                                         nonlinear=True))
+        f0 = g[f"{name}/forcing"]
+        F = np.stack([f0 * s for s in (1.0, 0.5, 2.0, 1.5)], axis=1)
+        f = torch.as_tensor(np.ascontiguousarray(F), device="cuda")
+        for kw in (dict(), dict(keep_state=True), dict(coarse=0)):
+            got = fm.fmg_solve(cfg, f, **kw)[0][:, 0].cpu().numpy()
+            assert np.array_equal(got, g[f"{name}/solution"]), (str(name), kw)
+
+
+@pytest.mark.slow
+def test_nonlinear_config3_full_size_reference_hash(fm):
+    """Config 3 at its full size (N = 2^20, 256 patches, b = 4, V(2,2), one SR
+    level, nonlinear): the hash-forcing column inside a 256-column batch (the
+    bench's batch shape and kernels) reproduces the reference-driver SHA-256."""
+    import hashlib
+
+    g = _nl_golden()
+    for name in g["hash_cases"]:
+        m0, m, n_sr, ns, _, P, b, salt = (int(x) for x in g[f"{name}/params"])
+        i = np.arange(2 ** m, dtype=np.uint64)
+        h = (i * np.uint64(2654435761) + np.uint64(salt)) % np.uint64(1 << 32)
+        f0 = float(g[f"{name}/scale"]) * (h.astype(np.float64) / float(1 << 32) - 0.5)
+        cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(m0, m), n_sr=n_sr,
+                              smoother=fm.SmootherConfig(ns=ns, n_patches=P, buffer=b,
+                                                         nonlinear=True))
+        B = 256
+        fcol = torch.as_tensor(f0, device="cuda")
+        f, _ = fm.nonlinear_batch(2 ** m, fm.nonlinear_scales(B, seed=7))
+        f[:, 5] = fcol
+        sol = fm.fmg_solve(cfg, f)[0]
+        got = sol[:, 5].cpu().numpy()
+        assert np.array_equal(got[:64], g[f"{name}/head"])
+        assert hashlib.sha256(np.ascontiguousarray(got).tobytes()).digest() == \
+            bytes(g[f"{name}/sha256"])

@@ -222,7 +222,7 @@ def _hash_rhs(n, salt):
 
 
 @pytest.mark.parametrize("case", ["h_c2", "h_c5_P256_b4", "h_c5_P16_b1", "h_c5_P1024_b8", "h_c4",
-                                  "h_c3lin", "h_c2_sr0", "h_c2_sr2"])
+                                  "h_c3lin", "h_c2_sr0", "h_c2_sr2", "h_c5_P64_b1", "h_c5_P16_b8"])
 def test_oracle_matches_reference_hashes_at_full_size(case):
     """The oracle against the reference's own solutions at the full BASELINE
     sizes of configs 2, 5 and 4 (N up to 2^24), for the machine-independent
@@ -236,3 +236,40 @@ def test_oracle_matches_reference_hashes_at_full_size(case):
     sol = O.fmg_solve(O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b), _hash_rhs(2 ** m, salt))
     assert np.array_equal(sol[:64], g[f"{case}/head"])
     assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == bytes(g[f"{case}/sha256"])
+
+
+# ---- nonlinear FAS pinned to the reference's own driver (oracle/gen_golden_nl.py) -------------
+_NL = os.path.join(os.path.dirname(__file__), "golden", "nonlinear.npz")
+
+
+def test_oracle_nonlinear_matches_reference_driver():
+    """The nonlinear restatement against the reference's OWN FMG driver, patch
+    assembly and Kaczmarz pass with the pointwise Newton-GS lane, the N(u) tau
+    and the Newton coarse solve injected through its lane registry and
+    module-level names (backends.py:22-47, cycles.py:22-28): bit for bit at
+    reduced sizes (V(1,1) .. V(3,3), SR depths 0-2, odd buffers)."""
+    from oracle import oracle as O
+
+    g = np.load(_NL)
+    for name in g["cases"]:
+        m0, m, n_sr, ns, _, P, b = (int(x) for x in g[f"{name}/params"])
+        cfg = O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b, nonlin=True)
+        got = O.fmg_solve(cfg, g[f"{name}/forcing"])
+        assert np.array_equal(got, g[f"{name}/solution"]), str(name)
+
+
+def test_oracle_nonlinear_config3_full_size_hash():
+    """Config 3's full geometry (N = 2^20, 256 patches, b = 4, V(2,2), n_sr = 1),
+    nonlinear, through the reference's driver: SHA-256 of the solution."""
+    import hashlib
+
+    from oracle import oracle as O
+
+    g = np.load(_NL)
+    for name in g["hash_cases"]:
+        m0, m, n_sr, ns, _, P, b, salt = (int(x) for x in g[f"{name}/params"])
+        f = float(g[f"{name}/scale"]) * _hash_rhs(2 ** m, salt)
+        sol = O.fmg_solve(O.make_cfg(m0, m, n_sr, ns, O.GEOM_PATCHES, P, b, nonlin=True), f)
+        assert np.array_equal(sol[:64], g[f"{name}/head"])
+        assert hashlib.sha256(np.ascontiguousarray(sol).tobytes()).digest() == \
+            bytes(g[f"{name}/sha256"])
