@@ -238,6 +238,17 @@ typedef struct fmgsr_plan_info {
 } fmgsr_plan_info;
 
 int fmgsr_plan_create(const fmgsr_plan_desc* desc, void** plan);
+/* Debug aids (compute-sanitizer stand-ins).  FMGSR_DEBUG_POISON: every solve
+ * first fills the plan's level fields, edge records and scratch with NaN, and
+ * after each FMG step fills the SR levels below it with NaN (the reference's
+ * debug_sr, cycles.py:161-165); a correct plan's results are unchanged.
+ * Setting flags drops the captured graphs.  fmgsr_plan_check_guards: with
+ * FMGSR_GUARDS=1 in the environment at plan creation every workspace array is
+ * bracketed by 4 KiB guard zones; *bad_bytes = guard bytes changed since
+ * (-1: the plan has no guards). */
+#define FMGSR_DEBUG_POISON 1
+int fmgsr_plan_set_debug(void* plan, int32_t flags);
+int fmgsr_plan_check_guards(void* plan, int64_t* bad_bytes);
 int fmgsr_plan_destroy(void* plan);
 int fmgsr_plan_get_info(void* plan, fmgsr_plan_info* info);
 /* One FMG-FAS(-SR) solve of B RHS: forcing, solution are DEVICE [2^m][ld]. */

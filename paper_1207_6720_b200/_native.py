@@ -97,6 +97,8 @@ _SIGS = {
     "fmgsr_manufactured_rhs_f64": (C.c_int, [_i64, _i64, _vp, _vp, _vp]),
     "fmgsr_plan_create": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_vp)]),
     "fmgsr_plan_destroy": (C.c_int, [_vp]),
+    "fmgsr_plan_set_debug": (C.c_int, [_vp, _i32]),
+    "fmgsr_plan_check_guards": (C.c_int, [_vp, C.POINTER(_i64)]),
     "fmgsr_plan_get_info": (C.c_int, [_vp, C.POINTER(PlanInfo)]),
     "fmgsr_plan_probe_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "fmgsr_plan_solve": (C.c_int, [_vp, _vp, _vp, _vp]),

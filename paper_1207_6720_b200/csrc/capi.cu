@@ -113,6 +113,8 @@ struct PlanBase {
   virtual void solve_host(const void* h_in, void* h_out, i64 ld_host, i64 chunks,
                           cudaStream_t s, int flags) = 0;
   virtual void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) = 0;
+  virtual void set_debug(int flags) = 0;
+  virtual i64 check_guards() = 0;
 };
 
 template <typename T>
@@ -120,6 +122,8 @@ struct Plan : PlanBase {
   struct Level {
     i64 n = 0, W = 0, b = 0;
     T* u[2] = {nullptr, nullptr};
+    void* ub[2] = {nullptr, nullptr};  // allocation bases of u[0], u[1] (debug poisoning)
+    size_t ubytes = 0;
     int cur = 0;
     T* f = nullptr;
     T* E = nullptr;
@@ -131,9 +135,23 @@ struct Plan : PlanBase {
   i64 sld = 0;
   int* cnt_all = nullptr;
   size_t cnt_bytes = 0;
-  std::vector<void*> allocs;
+  std::vector<void*> allocs;       // raw cudaMalloc pointers
+  std::vector<void*> alloc_user;   // what alloc() returned (after the front guard)
   std::vector<size_t> alloc_sizes;
-  i64 ws_bytes = 0;
+  // Debug aids in place of compute-sanitizer (closed on this pool):
+  //  guards (FMGSR_GUARDS=1 at plan creation): every workspace array sits
+  //    between two 4 KiB guard zones filled with 0x5A; check_guards() counts
+  //    changed guard bytes -- an out-of-bounds write detector;
+  //  FMGSR_DEBUG_POISON (fmgsr_plan_set_debug): every solve first fills the
+  //    level fields, edge records and scratch with NaN (uninitialised reads
+  //    would surface in the result), and after each FMG step fills the SR
+  //    levels below it with NaN -- the reference's debug_sr (cycles.py:161-165,
+  //    209-212): the only field a step may read from the previous one is the
+  //    previous finest level.
+  static constexpr size_t GUARD = 4096;
+  bool guards = false;
+  int debug = 0;
+  size_t n_field_allocs = 0;  i64 ws_bytes = 0;
   cudaStream_t cap = nullptr;
   std::map<std::pair<const void*, void*>, cudaGraphExec_t> graphs;
   // probe events around the finest-level top and up visits, recorded by every
@@ -211,9 +229,13 @@ struct Plan : PlanBase {
       return (T*)p;
     }
     void* p = nullptr;
-    check_cuda(cudaMalloc(&p, bytes ? bytes : 16), "plan workspace cudaMalloc");
+    const size_t ub = bytes ? bytes : 16, g = guards ? GUARD : 0;
+    check_cuda(cudaMalloc(&p, ub + 2 * g), "plan workspace cudaMalloc");
     allocs.push_back(p);
-    alloc_sizes.push_back(bytes ? bytes : 16);
+    if (g) check_cuda(cudaMemset(p, 0x5A, ub + 2 * g), "guard fill");
+    p = (char*)p + g;
+    alloc_user.push_back(p);
+    alloc_sizes.push_back(ub);
     ws_bytes += (i64)bytes;
     return (T*)p;
   }
@@ -224,6 +246,8 @@ struct Plan : PlanBase {
                 bool local_ = false) {
     dry = dry_;
     local = local_;
+    const char* ge = getenv("FMGSR_GUARDS");
+    guards = !dry && ge && ge[0] == '1';
     try {
       init(desc, shards, shard);
     } catch (...) {
@@ -362,6 +386,9 @@ struct Plan : PlanBase {
         size_t fb = (size_t)rows * ld * sizeof(T);
         L.u[0] = alloc(fb) + shift;
         L.u[1] = alloc(fb) + shift;
+        L.ub[0] = L.u[0] - shift;
+        L.ub[1] = L.u[1] - shift;
+        L.ubytes = fb;
         if (l < m) L.f = alloc(fb) + shift;
         else fm = alloc(fb) + shift;
         ob[l] = alloc((size_t)10 * Bp * sizeof(T));
@@ -370,6 +397,9 @@ struct Plan : PlanBase {
         size_t fb = (size_t)L.n * ld * sizeof(T);
         L.u[0] = alloc(fb);
         L.u[1] = alloc(fb);
+        L.ub[0] = L.u[0];
+        L.ub[1] = L.u[1];
+        L.ubytes = fb;
         if (l < m) L.f = alloc(fb);
       }
       if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
@@ -382,12 +412,13 @@ struct Plan : PlanBase {
       sld = Bp;
       scratch = alloc((size_t)scratch_rows * sld * sizeof(T));
     }
+    n_field_allocs = allocs.size();  // everything so far is rewritten before it is read
     cnt_bytes = (size_t)cnt_total * sizeof(int);
     cnt_all = (int*)alloc(cnt_bytes);
     if (!dry) check_cuda(cudaMemset(cnt_all, 0, cnt_bytes ? cnt_bytes : 16), "plan memset");
     if (local)  // no halo ever arrives: keep the never-written rows finite
       for (size_t k = 0; k < allocs.size(); k++)
-        check_cuda(cudaMemset(allocs[k], 0, alloc_sizes[k]), "plan memset");
+        check_cuda(cudaMemset(alloc_user[k], 0, alloc_sizes[k]), "plan memset");
     i64 off = 0;
     for (int l = m0 + 1; l <= m; l++) {
       Level& L = lv[l];
@@ -462,6 +493,7 @@ struct Plan : PlanBase {
     if (!dry)
       for (void* p : allocs) cudaFree(p);
     allocs.clear();
+    alloc_user.clear();
     alloc_sizes.clear();
   }
 
@@ -864,6 +896,7 @@ struct Plan : PlanBase {
   void enqueue(const T* forcing, T* solution, cudaStream_t s) {
     const int m0 = d.m0, m = d.m;
     reset_state(s);
+    poison_all(s);
     if (use_coarse) {
       enqueue_coarse(forcing, solution, s);
       return;
@@ -884,6 +917,7 @@ struct Plan : PlanBase {
         const T* fl = (l == m) ? forcing : lv[l].f;
         visit_up(l, fl, (l == m && t == m) ? solution : nullptr, s, l == m && t == m);
       }
+      poison_sr_below(t, s);
     }
   }
 
@@ -1147,6 +1181,41 @@ struct Plan : PlanBase {
   void* ncomm = nullptr;
   void comm_nccl(const Step& st, cudaStream_t s);  // defined after NcclApi
 
+  void poison_all(cudaStream_t s) {
+    if (dry || !(debug & FMGSR_DEBUG_POISON)) return;
+    for (size_t k = 0; k < n_field_allocs; k++)
+      check_cuda(cudaMemsetAsync(alloc_user[k], 0xFF, alloc_sizes[k], s), "poison");
+  }
+  // after FMG step t: the SR levels below t are dead (levels <= Lc live on chip)
+  void poison_sr_below(int t, cudaStream_t s) {
+    if (dry || !(debug & FMGSR_DEBUG_POISON)) return;
+    for (int l = d.m0; l < t; l++)
+      if (is_sr(l) && !(use_coarse && l <= Lc))
+        for (int k = 0; k < 2; k++)
+          check_cuda(cudaMemsetAsync(lv[l].ub[k], 0xFF, lv[l].ubytes, s), "poison SR level");
+  }
+  i64 check_guards() override {
+    if (!guards) return -1;
+    std::vector<unsigned char> h(GUARD);
+    i64 bad = 0;
+    for (size_t k = 0; k < allocs.size(); k++) {
+      const char* lo = (const char*)allocs[k];
+      const char* hi = (const char*)alloc_user[k] + alloc_sizes[k];
+      for (const char* z : {lo, hi}) {
+        check_cuda(cudaMemcpy(h.data(), z, GUARD, cudaMemcpyDeviceToHost), "guard read");
+        for (unsigned char c : h) bad += c != 0x5A;
+      }
+    }
+    return bad;
+  }
+  void set_debug(int flags) override {
+    debug = flags;
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);  // recapture with the new flags
+    graphs.clear();
+    for (auto& kv : fgraphs) cudaGraphExecDestroy(kv.second);
+    fgraphs.clear();
+  }
+
   void reset_state(cudaStream_t s) {
     n_launch = 0;
     n_visit = 0;
@@ -1161,6 +1230,7 @@ struct Plan : PlanBase {
     for (const Step& st : steps()) {
       run_step(st, forcing, solution, s);
       if (S > 1) comm_nccl(st, s);
+      if (st.kind == ST_UP && st.l == st.t) poison_sr_below(st.t, s);
     }
   }
 
@@ -1962,6 +2032,19 @@ int fmgsr_plan_create(const fmgsr_plan_desc* desc, void** plan) {
     if (desc->dtype == 0) p = new Plan<double>(*desc);
     else p = new Plan<float>(*desc);
     *plan = p;
+  });
+}
+int fmgsr_plan_set_debug(void* plan, int32_t flags) {
+  return guarded([&] {
+    require(plan != nullptr, "plan_set_debug: null plan");
+    require((flags & ~FMGSR_DEBUG_POISON) == 0, "plan_set_debug: unknown flags");
+    reinterpret_cast<PlanBase*>(plan)->set_debug(flags);
+  });
+}
+int fmgsr_plan_check_guards(void* plan, int64_t* bad_bytes) {
+  return guarded([&] {
+    require(plan && bad_bytes, "plan_check_guards: null argument");
+    *bad_bytes = reinterpret_cast<PlanBase*>(plan)->check_guards();
   });
 }
 int fmgsr_plan_destroy(void* plan) {

@@ -174,6 +174,22 @@ class FmgPlan:
             N.check(N.lib().fmgsr_plan_probe_ms(self._h, C.byref(t), C.byref(u)), "plan_probe_ms")
         return t.value, u.value
 
+    def set_debug(self, poison: bool = True) -> None:
+        """NaN-poison mode (fmgsr_plan_set_debug FMGSR_DEBUG_POISON): every solve
+        fills the workspace fields with NaN first and the SR levels below each
+        finished FMG step after it (the reference's debug_sr); results of a
+        correct plan are unchanged."""
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_set_debug(self._h, 1 if poison else 0), "plan_set_debug")
+
+    def check_guards(self) -> int:
+        """Changed guard bytes around the workspace arrays (plans created with
+        FMGSR_GUARDS=1; -1 without guards)."""
+        bad = C.c_int64()
+        with self._lock:
+            N.check(N.lib().fmgsr_plan_check_guards(self._h, C.byref(bad)), "plan_check_guards")
+        return bad.value
+
     def info(self) -> dict:
         inf = N.PlanInfo()
         with self._lock:
