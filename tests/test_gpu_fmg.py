@@ -389,3 +389,4 @@ def test_plan_probe_events_time_the_finest_visits(fm):
     if whole.info()["coarse_cutoff"] == 10:
         assert whole.probe_ms() == (-1.0, -1.0)
 
+

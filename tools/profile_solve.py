@@ -19,8 +19,14 @@ ap.add_argument("--workload", default="config2")
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--graph", action="store_true")
 ap.add_argument("--unfused", action="store_true")
+ap.add_argument("--P", type=int, default=0, help="override the patch count")
+ap.add_argument("--b", type=int, default=-1, help="override the buffer")
 a = ap.parse_args()
-w = bench.WORKLOADS[a.workload]
+w = dict(bench.WORKLOADS[a.workload])
+if a.P:
+    w["P"] = a.P
+if a.b >= 0:
+    w["b"] = a.b
 dt = torch.float64 if w["dtype"] == "f64" else torch.float32
 nl = bool(w.get("nonlinear", False))
 cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
