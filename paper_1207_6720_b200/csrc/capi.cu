@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
@@ -571,7 +573,17 @@ struct Plan : PlanBase {
     else
       check_cuda(cudaEventRecord(e, s), "probe record");
   }
+  // NVTX range per level visit ("T_24", "D_23", "U_24", "C_12", "F_24", "X_3"),
+  // so ncu --nvtx --nvtx-include "U_20/" picks one visit of an op-by-op solve
+  void nvtx_push(int lvl, int kind) const {
+    if (dry) return;
+    static const char kc[] = {'T', 'D', 'U', 'X', 'F', 'C'};
+    char name[16];
+    snprintf(name, sizeof name, "%c_%d", kc[kind], lvl);
+    nvtxRangePushA(name);
+  }
   void mark_begin(cudaStream_t s, int lvl, int kind) {
+    nvtx_push(lvl, kind);
     n_visit++;
     probe_open = -1;
     if (lvl == d.m && (kind == VK_TOP || kind == VK_UP) && probe_ev[0][0] && !dry) {
@@ -587,6 +599,7 @@ struct Plan : PlanBase {
     ev_kind.push_back(kind);
   }
   void mark_end(cudaStream_t s) {
+    if (!dry) nvtxRangePop();
     if (probe_open >= 0) {
       probe_record(probe_ev[probe_open][1], s);
       probe_open = -1;

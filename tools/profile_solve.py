@@ -21,6 +21,8 @@ ap.add_argument("--graph", action="store_true")
 ap.add_argument("--unfused", action="store_true")
 ap.add_argument("--P", type=int, default=0, help="override the patch count")
 ap.add_argument("--b", type=int, default=-1, help="override the buffer")
+ap.add_argument("--shards", type=int, default=0, help="run shard --rank of an S-way split")
+ap.add_argument("--rank", type=int, default=0)
 a = ap.parse_args()
 w = dict(bench.WORKLOADS[a.workload])
 if a.P:
@@ -32,11 +34,19 @@ nl = bool(w.get("nonlinear", False))
 cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_sr"],
                       smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
                                                  nonlinear=nl))
-plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused, use_graph=a.graph))
+if not a.shards:
+    plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused,
+                                          use_graph=a.graph))
 if nl:
     f, _ = fm.nonlinear_batch(2 ** w["m"], fm.nonlinear_scales(w["B"]), dt)
 else:
     f, _ = fm.fourier_batch(2 ** w["m"], fm.fourier_coefficients(w["B"]), dt, with_exact=False)
+if a.shards:  # one shard's local plan (transfers stubbed), op by op unless --graph
+    from paper_1207_6720_b200.shard import LocalShardPlan
+
+    plan = LocalShardPlan(cfg, w["B"], a.shards, a.rank, dt, use_graph=a.graph)
+    rows = 2 ** w["m"] // a.shards
+    f = f[a.rank * rows:(a.rank + 1) * rows].contiguous()
 sol = torch.empty_like(f)
 for _ in range(a.solves):
     plan.solve(f, sol)
