@@ -68,10 +68,12 @@ struct Chain {
       for (int k = 0; k < R; k++) bulk_g2s(dst + k * NT, p[k], 32 * sizeof(T), bar);
     }
   }
-  // wait until pair g has landed in its slot
+  // wait until pair g has landed in its slot; AHEAD = g - (the pair whose
+  // cells are being updated): pairs up to that pair + D - 1 have been staged
+  template <int AHEAD = 1>
   __device__ __forceinline__ void await(i64 g) {
     if (!BULK) {
-      cp_wait<D - 2>();
+      cp_wait<D - 1 - AHEAD>();
       return;
     }
     mbar_wait(bars + (g & (D - 1)), (unsigned)(((g - x0) / D) & 1));
@@ -126,51 +128,207 @@ struct Chain {
     f1 = r.f1;
   }
 
-  // interior pairs [q, q_end]: OWNED selects store/epilogue
-  template <bool OWNED>
-  __device__ __forceinline__ void run_fast(i64 q, i64 q_end) {
-    if (!BULK) src.fast_ptrs(q + D);
-    T* po = (OWNED && out) ? out + (2 * q) * ld : nullptr;
-    if (EPI && OWNED) epi->fast_begin(q);
-    const bool st_u = OWNED && out && store;
-    const T* pw = (FUNC && OWNED && fw) ? fw + (2 * q) * ld : nullptr;
-#pragma unroll 2
-    for (; q <= q_end; q++) {
-      await(q + 1);
-      Raw<T> r = src.template fetch<NT>(slot(q + 1));
+  // Fast-loop iteration for pair q with a one-pair lookahead (WIDE shape):
+  // wait for pair q+1, stage pair q+D, build pair q+1's smoother input and
+  // run the two Gauss-Seidel cells of pair q.
+  template <bool KP2>
+  __device__ __forceinline__ void it1(i64 q, T& n0, T& n1, T& e0, T& e1) {
+    await<1>(q + 1);
+    Raw<T> r = src.template fetch<NT>(slot(q + 1));
+    if (BULK) {
+      stage(q + D);
+    } else {
+      src.template issue_fast<NT>(slot(q));
+      cp_commit();
+    }
+    T w0, w1;
+    src.template make_fast<KP2>(r, w0, w1);
+    n0 = gsi(uL, v0, v1, f0);
+    n1 = gsi(n0, v1, w0, f1);
+    e0 = f0;
+    e1 = f1;
+    uL = n1;
+    v0 = w0;
+    v1 = w1;
+    f0 = r.f0;
+    f1 = r.f1;
+  }
+
+  // Fast-loop iteration for pair q with a two-deep lookahead (DEEP shape: a
+  // warp issuing alone, where the build of the next pair must not sit between
+  // the chain's dependent operations): on entry
+  // (v0, v1, f0, f1) is pair q's smoother input and (w0, w1, g0, g1) pair
+  // q+1's.  AHEAD: wait for, fetch and build pair q+2 (not on the last pair of
+  // the loop, which leaves the source exactly where step_slow expects it).
+  // The build of pair q+2 does not depend on the Gauss-Seidel chain of pair
+  // q, so the two overlap.  Stages pair q+D into the slot pair q came from.
+  // Returns the smoothed cells (n0, n1) and pair q's f (e0, e1).
+  template <bool AHEAD, bool KP2>
+  __device__ __forceinline__ void it2(i64 q, T& w0, T& w1, T& g0, T& g1, T& n0, T& n1, T& e0,
+                                      T& e1) {
+    T x0, x1, h0, h1;
+    if (AHEAD) {
+      await<2>(q + 2);
+      Raw<T> r = src.template fetch<NT>(slot(q + 2));
       if (BULK) {
         stage(q + D);
       } else {
         src.template issue_fast<NT>(slot(q));
         cp_commit();
       }
-      T w0, w1;
-      src.make_fast(r, w0, w1);
-      T n0 = gsi(uL, v0, v1, f0);
-      T n1 = gsi(n0, v1, w0, f1);
-      uL = n1;
-      if (OWNED) {
-        if (FUNC) {
-          if (pw) {
-            facc = xadd(facc, xmul(pw[0], n0));
-            facc = xadd(facc, xmul(pw[ld], n1));
-            pw += 2 * ld;
-          } else {
-            facc = xadd(facc, n0);
-            facc = xadd(facc, n1);
-          }
-        } else if (st_u) {
-          po[0] = n0;
-          po[ld] = n1;
-        }
-        if (po) po += 2 * ld;
-        if (EPI) epi->push_fast(n0, n1, f0, f1, store);
+      src.template make_fast<KP2>(r, x0, x1);
+      h0 = r.f0;
+      h1 = r.f1;
+    } else {
+      if (BULK) {
+        stage(q + D);
+      } else {
+        src.template issue_fast<NT>(slot(q));
+        cp_commit();
       }
-      v0 = w0;
-      v1 = w1;
-      f0 = r.f0;
-      f1 = r.f1;
     }
+    n0 = gsi(uL, v0, v1, f0);
+    n1 = gsi(n0, v1, w0, f1);
+    e0 = f0;
+    e1 = f1;
+    uL = n1;
+    v0 = w0;
+    v1 = w1;
+    f0 = g0;
+    f1 = g1;
+    if (AHEAD) {
+      w0 = x0;
+      w1 = x1;
+      g0 = h0;
+      g1 = h1;
+    }
+  }
+
+  // interior pairs [q, q_end]: OWNED selects store/epilogue, WU the store of
+  // the smoothed cells, WUH the epilogue's store of R u.  The epilogue of pair
+  // q runs one pair late, inside iteration q+1: its operations depend only on
+  // finished values, so they fill the dependency gaps of the next pair's
+  // Gauss-Seidel chain instead of waiting on it (the arithmetic of every value
+  // is unchanged).  The loop body is one basic block: no per-lane or uniform
+  // branches (stores are unconditional, see visit_kernel's rr).
+  template <bool OWNED, bool WU, bool WUH, bool KP2>
+  __device__ __forceinline__ void run_fast(i64 q, i64 q_end) {
+    if (q > q_end) return;
+    if (!BULK) src.fast_ptrs(q + D);
+    T* po = (OWNED && WU) ? out + (2 * q) * ld : nullptr;
+    const T* pw = (FUNC && OWNED && fw) ? fw + (2 * q) * ld : nullptr;
+    auto emit = [&](T n0, T n1) {
+      if (FUNC && OWNED) {
+        if (pw) {
+          facc = xadd(facc, xmul(pw[0], n0));
+          facc = xadd(facc, xmul(pw[ld], n1));
+          pw += 2 * ld;
+        } else {
+          facc = xadd(facc, n0);
+          facc = xadd(facc, n1);
+        }
+      } else if (OWNED && WU) {
+        po[0] = n0;
+        po[ld] = n1;
+        po += 2 * ld;
+      }
+    };
+    if constexpr (D < 16) {  // one-pair lookahead
+      if (EPI && OWNED) {
+        epi->fast_begin(q);
+        T p0, p1, pf0, pf1;  // the pair whose epilogue is pending
+        it1<KP2>(q, p0, p1, pf0, pf1);
+        emit(p0, p1);
+        for (q++; q <= q_end; q++) {
+          T n0, n1, e0, e1;
+          epi->template push_fast<WUH>(p0, p1, pf0, pf1);
+          it1<KP2>(q, n0, n1, e0, e1);
+          emit(n0, n1);
+          p0 = n0;
+          p1 = n1;
+          pf0 = e0;
+          pf1 = e1;
+        }
+        epi->template push_fast<WUH>(p0, p1, pf0, pf1);
+        return;
+      }
+#pragma unroll 2
+      for (; q <= q_end; q++) {
+        T n0, n1, e0, e1;
+        it1<KP2>(q, n0, n1, e0, e1);
+        emit(n0, n1);
+      }
+      return;
+    }
+    // two-pair lookahead: pair q+1 ahead of the loop
+    T w0, w1, g0, g1;
+    await<1>(q + 1);
+    {
+      Raw<T> r = src.template fetch<NT>(slot(q + 1));
+      src.template make_fast<KP2>(r, w0, w1);
+      g0 = r.f0;
+      g1 = r.f1;
+    }
+    if (EPI && OWNED) {
+      epi->fast_begin(q);
+      T p0, p1, pf0, pf1;  // the pair whose epilogue is pending
+      if (q == q_end) {
+        it2<false, KP2>(q, w0, w1, g0, g1, p0, p1, pf0, pf1);
+      } else {
+        it2<true, KP2>(q, w0, w1, g0, g1, p0, p1, pf0, pf1);
+        emit(p0, p1);
+#pragma unroll 2
+        for (q++; q < q_end; q++) {
+          T n0, n1, e0, e1;
+          epi->template push_fast<WUH>(p0, p1, pf0, pf1);
+          it2<true, KP2>(q, w0, w1, g0, g1, n0, n1, e0, e1);
+          emit(n0, n1);
+          p0 = n0;
+          p1 = n1;
+          pf0 = e0;
+          pf1 = e1;
+        }
+        T n0, n1, e0, e1;
+        epi->template push_fast<WUH>(p0, p1, pf0, pf1);
+        it2<false, KP2>(q, w0, w1, g0, g1, n0, n1, e0, e1);
+        p0 = n0;
+        p1 = n1;
+        pf0 = e0;
+        pf1 = e1;
+      }
+      emit(p0, p1);
+      epi->template push_fast<WUH>(p0, p1, pf0, pf1);
+      return;
+    }
+#pragma unroll 2
+    for (; q < q_end; q++) {
+      T n0, n1, e0, e1;
+      it2<true, KP2>(q, w0, w1, g0, g1, n0, n1, e0, e1);
+      emit(n0, n1);
+    }
+    T n0, n1, e0, e1;
+    it2<false, KP2>(q, w0, w1, g0, g1, n0, n1, e0, e1);
+    emit(n0, n1);
+  }
+  template <bool OWNED, bool KP2>
+  __device__ __forceinline__ void run_fast_k(i64 q, i64 q_end) {
+    if (!OWNED) {
+      run_fast<false, false, false, KP2>(q, q_end);
+    } else if (EPI) {
+      const bool wu = out != nullptr, wuh = epi->write_uH;
+      if (wu && wuh) run_fast<true, true, true, KP2>(q, q_end);
+      else if (wu) run_fast<true, true, false, KP2>(q, q_end);
+      else if (wuh) run_fast<true, false, true, KP2>(q, q_end);
+      else run_fast<true, false, false, KP2>(q, q_end);
+    } else {
+      if (out) run_fast<true, true, false, KP2>(q, q_end);
+      else run_fast<true, false, false, KP2>(q, q_end);
+    }
+  }
+  template <bool OWNED>
+  __device__ __forceinline__ void run_fast_any(i64 q, i64 q_end) {
+    if (!CR || src.kz.pow2) run_fast_k<OWNED, true>(q, q_end);
+    else run_fast_k<OWNED, false>(q, q_end);
   }
 
   __device__ __forceinline__ void run(i64 we) {
@@ -208,14 +366,14 @@ struct Chain {
     const i64 bl = lo, bh = hi < oq - 1 ? hi : oq - 1;
     if (bl <= bh) {
       for (; q < bl; q++) step_slow(q);
-      run_fast<false>(q, bh);
+      run_fast_any<false>(q, bh);
       q = bh + 1;
     }
     // owned cells
     const i64 ol = lo > oq + (EPI ? 2 : 0) ? lo : oq + (EPI ? 2 : 0);
     if (ol <= hi) {
       for (; q < ol; q++) step_slow(q);
-      run_fast<true>(q, hi);
+      run_fast_any<true>(q, hi);
       q = hi + 1;
     }
     for (; q <= qe; q++) step_slow(q);

@@ -211,6 +211,15 @@ __device__ __forceinline__ T gs_int_o(const GsCoef<T>& c, T uL, T u, T uR, T f) 
 // _kernels_numba.py:53-56: r = uc - 0.5(a+b); t = r/proj_diag; a,b += 0.5 t.
 // When proj_diag is a power of two (the reference's 0.5) the division is an
 // exact multiply by its reciprocal.
+// KP2: proj_diag is known to be a power of two (no division code at all)
+template <bool KP2, typename T>
+__device__ __forceinline__ void kaczmarz_pair_k(T& a, T& b, T uc, const KzCoef<T>& k) {
+  T r = xsub(uc, xmul(T(0.5), xadd(a, b)));
+  T t = KP2 ? xmul(r, k.recip) : xdiv(r, k.proj_diag);
+  T h = xmul(T(0.5), t);
+  a = xadd(a, h);
+  b = xadd(b, h);
+}
 template <typename T>
 __device__ __forceinline__ void kaczmarz_pair(T& a, T& b, T uc, const KzCoef<T>& k) {
   T r = xsub(uc, xmul(T(0.5), xadd(a, b)));
@@ -513,7 +522,10 @@ struct PairSource {
     if (CR && q >= wlo && q < whi) kaczmarz_pair(v0, v1, target, kz);
   }
 
-  // interior-only make (no boundary rows; CR pair always inside the window)
+  // interior-only make (no boundary rows; CR pair always inside the window);
+  // KP2: the Kaczmarz divisor is a power of two (the fast loops are unswitched
+  // on it, so their bodies stay branch-free)
+  template <bool KP2 = false>
   __device__ __forceinline__ void make_fast(const Raw<T>& r, T& v0, T& v1) {
     T target = r.g;
     if (SRC == SRC_LOAD) {
@@ -538,7 +550,10 @@ struct PairSource {
       s2 = s3;
       s3 = r.h;
     }
-    if (CR) kaczmarz_pair(v0, v1, target, kz);
+    if (CR) {
+      if (KP2) kaczmarz_pair_k<true>(v0, v1, target, kz);
+      else kaczmarz_pair(v0, v1, target, kz);
+    }
   }
 };
 
@@ -608,15 +623,19 @@ struct Epilogue {
     puH = uH_out ? uH_out + j * ld : nullptr;
     pfH = fH_out + (j - 1) * ld;
   }
-  __device__ __forceinline__ void push_fast(T a, T b, T f0, T f1, bool store) {
+  // WUH: store R u (uniform per launch); every lane stores (visit_kernel's rr)
+  template <bool WUH>
+  __device__ __forceinline__ void push_fast(T a, T b, T f0, T f1) {
     T Rj = xmul(T(0.5), xadd(a, b));
     T Rfj = xmul(T(0.5), xadd(f0, f1));
-    if (write_uH && store) *puH = Rj;
-    puH += ld;
+    if (WUH) {
+      *puH = Rj;
+      puH += ld;
+    }
     T Lodd = xmul(xsub(xsub(xmul(T(2), up1), up2), a), inv_h2);
     T RL = xmul(T(0.5), xadd(Lprev, Lodd));
     T LH = xmul(xsub(xsub(xmul(T(2), Rm1), Rm2), Rj), inv_H2);
-    if (store) *pfH = xadd(Rfm1, xsub(LH, RL));
+    *pfH = xadd(Rfm1, xsub(LH, RL));
     pfH += ld;
     Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);
     up2 = a;

@@ -20,14 +20,42 @@
 
 namespace fmgsr {
 
-// FMGSR_VISIT_CPL=1 forces one RHS column per lane (A/B tests)
-static bool visit_cpl2_enabled() {
+// Lane width (RHS columns per lane).  FMGSR_VISIT_CPL=1 forces one column per
+// lane, =2 two columns wherever legal; default: automatic (visit_lanes_auto).
+static int visit_cpl_env() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FMGSR_VISIT_CPL");
-    v = (e && std::string(e) == "1") ? 0 : 1;
+    v = (e && std::string(e) == "1") ? 1 : (e && std::string(e) == "2") ? 2 : 0;
   }
-  return v == 1;
+  return v;
+}
+static bool visit_cpl2_enabled() { return visit_cpl_env() != 1; }
+
+// SM sub-partitions (warp schedulers) of the device the launch runs on
+int visit_smsps() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    n = 4 * sms;
+  }
+  return n;
+}
+
+// A visit is issue-latency bound when its chains cannot fill the GPU: one lane
+// runs one sequential chain, so with at most one warp per SM sub-partition
+// every warp issues alone and a pair costs its own instruction count (about
+// 2 x 50 fp64 issue cycles per pair with two columns per lane).  One column
+// per lane then halves each warp's instructions per pair and doubles the
+// number of sub-partitions at work (config-5 P = 16 / 64).  With more chains
+// than that, two columns per lane move the same bytes with fewer instructions.
+template <typename T>
+static bool visit_few_chains(const VisitDesc<T>& d) {
+  const i64 P = d.olo ? d.P : (d.p_count >= 0 ? d.p_count : d.n / d.W);
+  const i64 warps1 = P * ((d.B + 31) / 32);
+  return warps1 <= visit_smsps();
 }
 
 // the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
@@ -36,8 +64,10 @@ template <typename TV, typename T, int SHAPE>
 void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s);
 
 // Two columns per lane: whole 64-column row groups, 2-element-aligned rows
-// and pointers, uniform geometry on the whole level (no explicit patch
-// arrays, no shard slab: their edge outboxes keep the scalar layout).
+// and pointers, uniform geometry (no explicit patch arrays).  A shard slab's
+// edge outbox [2][5][ldE] has the same memory layout with either lane type
+// once B % 64 == 0 (ldE = B doubles = 2 x the V2 stride), so the slab-edge
+// fix-up and the transfers are unchanged.
 // Measured on config 2 (tools/visit_breakdown.py): mid-level visits 10-25 %
 // faster, 3.29 -> 3.08 ms per cycle; config 5 fp32 8.66 -> 6.84 ms.
 template <typename T>
@@ -48,9 +78,9 @@ static bool visit_cpl2_ok(const VisitDesc<T>& d) {
   // lane (U_16 of config 2: 270 vs 226 us; 16-byte lanes need ~220 registers
   // there); every other visit kind, and every fp32 visit, is faster
   if (sizeof(T) == 8 && d.src == SRC_FMG && d.cr) return false;
-  return visit_cpl2_enabled() && d.B % 64 == 0 && d.ld % 2 == 0 && !d.olo && d.p_count < 0 &&
-         !d.left_remote && !d.right_remote && al(d.u_src) && al(d.uH) && al(d.uc) && al(d.f) &&
-         al(d.u_out) && al(d.uH_out) && al(d.fH_out) && al(d.E) && al(d.fun_w) &&
+  if (visit_cpl_env() == 0 && visit_few_chains(d)) return false;
+  return visit_cpl2_enabled() && d.B % 64 == 0 && d.ld % 2 == 0 && !d.olo && al(d.u_src) && al(d.uH) && al(d.uc) && al(d.f) &&
+         al(d.u_out) && al(d.uH_out) && al(d.fH_out) && al(d.E) && al(d.E_out) && al(d.fun_w) &&
          al(d.fun_part);
 }
 
@@ -82,11 +112,8 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
-  // one launch shape (128-thread CTAs, 8-pair ring): one-warp CTAs with a
-  // 16-pair ring (VisitShape NARROW) measured slower on every few-chain case
-  // tried (config-5 P = 16: 63.1 vs 44.2 ms per cycle; an 8-way shard of
-  // config 4: 9.37 vs 8.76 ms) -- DESIGN.md 6c
   if (visit_cpl2_ok(d)) visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
+  else if (visit_few_chains(d)) visit_fill_launch<T, T, SHAPE_DEEP>(d, s);
   else visit_fill_launch<T, T, SHAPE_WIDE>(d, s);
   check_launch("visit_kernel");
 }

@@ -32,14 +32,14 @@ struct VisitArgs {
 };
 
 // Launch shapes of the visit kernel (threads per CTA, cp.async ring depth in
-// pairs per lane).  WIDE: 128-thread CTAs, 8-pair ring -- many chains per SM
-// (the large levels at B >= 64).  NARROW: one-warp CTAs, 16-pair ring -- few
-// chains per SM (small P x B: config-5 P = 16, one shard's slab of an S-way
-// split): the warps spread over every SM instead of leaving SMs idle behind
-// 4-warp CTAs, and each lane keeps twice the bytes in flight.
+// pairs per lane).  WIDE: 8-pair ring -- many chains per SM (the large levels
+// at B >= 64), where other warps hide each lane's memory latency.  DEEP:
+// 16-pair ring -- few chains (at most one warp per SM sub-partition, scalar
+// lanes: config-5 P = 16 / 64): a warp issues alone, so its own ring must
+// cover the DRAM latency while the fast loop fetches two pairs ahead.
 template <int SHAPE>
 struct VisitShape {
-  static constexpr int NT = SHAPE == SHAPE_WIDE ? 128 : 32;
+  static constexpr int NT = 128;
   static constexpr int D = SHAPE == SHAPE_WIDE ? 8 : 16;
 };
 
@@ -56,14 +56,20 @@ template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool F
 __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_kernel(const VisitArgs<T> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
-  const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 pl = gw / a.nrg;  // patch index within the launched range
-  const int rg = (int)(gw - pl * a.nrg);
+  // 32-bit index math (a launch has < 2^32 threads): no 64-bit division at entry
+  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nrg = (unsigned)a.nrg;
+  const unsigned pl32 = nrg == 1 ? gw : gw / nrg;
+  const int rg = (int)(gw - pl32 * nrg);
+  const i64 pl = pl32;  // patch index within the launched range
   if (pl >= a.P) return;  // warp-uniform
   const i64 p = a.p_begin + pl;
   const int r = rg * 32 + lane;
-  const bool store = r < a.B;
-  const int rr = store ? r : a.B - 1;
+  // Lanes past the last RHS column run column B-1's chain (rr) and write its
+  // bit-identical values to column B-1, so every store is unconditional and
+  // the chain's fast loop has no per-lane branches.
+  const bool store = true;
+  const int rr = r < a.B ? r : a.B - 1;
 
   i64 os, oe, ws, we;
   if (a.olo) {
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
   ch.oe = oe;
   ch.store = store;
   ch.ring = reinterpret_cast<T*>(visit_smem) + threadIdx.x;
-  ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + r : nullptr;
+  ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + rr : nullptr;
   ch.fw = (FUNC && a.fun_w) ? a.fun_w + rr : nullptr;
   ch.facc = T(0);
   if (!EPI) {
@@ -123,8 +129,8 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
   ep.left_dom = (os == 0);
   ep.right_dom = (oe == a.n);
   ep.write_uH = a.uH_out != nullptr;
-  ep.uH_out = a.uH_out ? a.uH_out + r : nullptr;
-  ep.fH_out = a.fH_out + r;
+  ep.uH_out = a.uH_out ? a.uH_out + rr : nullptr;
+  ep.fH_out = a.fH_out + rr;
   ep.ld = a.ld;
   ep.nc = a.nc;
   ep.cnt = 0;
@@ -196,7 +202,11 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   // every config (config 2 / 4 / 5: +0.3 / +1.5 / +1.6 % per cycle), and fp32
   // lanes likewise (config 5 fp32: level-19 up 452 -> 379 us)
   constexpr bool bulk_lanes = std::is_same<T, double>::value;
-  const bool bulk = bulk_lanes && SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && bulk_ok(a);
+  // and only with more warps than SM sub-partitions: a warp issuing alone
+  // waits on lane 0's serial bulk issue every pair (an 8-way shard of config 4,
+  // U_23 with scalar lanes: 19 % of the stall samples on the mbarrier wait)
+  const bool many = a.P * a.nrg > visit_smsps();
+  const bool bulk = bulk_lanes && SrcRows<SRC, CR>::R >= 5 && a.W >= 64 && many && bulk_ok(a);
   // functional output of the final up visit (non-SR: FAS correction; SR: Pi + CR)
   if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
     if (a.fun_part) {

@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
     (13, 256, 8, 1, 32, 8, 6),    # config-4 style buffer, 8 shards
     (12, 32, 3, 0, 96, 4, 6),     # odd buffer, no SR, B not a power of two
     (12, 64, 1, 2, 64, 2, 6),     # b = 1 and two SR levels
+    (13, 256, 8, 1, 128, 8, 6),   # two RHS columns per lane on the slabs, 8 shards
 ])
 def test_shard_group_matches_unsharded(fm, m, P, b, n_sr, B, shards, coarse):
     from paper_1207_6720_b200.shard import ShardGroup
