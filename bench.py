@@ -46,12 +46,27 @@ WORKLOADS = {
     "config1": dict(m0=3, m=10, P=4, b=2, ns=1, n_sr=1, B=1, dtype="f64"),
     "config5": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f64"),
     "config5_f32": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f32"),
+    # the same fp32 fields (same HBM bytes) with fp64 arithmetic
+    "config5_f32f64": dict(m0=3, m=20, P=256, b=4, ns=1, n_sr=1, B=256, dtype="f32",
+                           arith="f64"),
     # BASELINE config 3: -u'' + u^3 = f, V(2,2), manufactured RHS scaled per RHS
     "config3": dict(m0=3, m=20, P=256, b=4, ns=2, n_sr=1, B=256, dtype="f64", nonlinear=True),
 }
 DEFAULT_WORKLOAD = "config4"
 METRIC = "fine-grid unknowns solved/sec (one FMG-FAS-SR cycle)"
 UNIT = "unknowns/s"
+
+
+def _arith(w):
+    """Arithmetic dtype of a workload (None: the field dtype)."""
+    import torch
+
+    return torch.float64 if w.get("arith") == "f64" else None
+
+
+def dtype_label(w) -> str:
+    """The JSON line's dtype: the arithmetic type (and the storage when narrower)."""
+    return "f64 (f32 fields)" if w.get("arith") == "f64" else w["dtype"]
 
 
 def throughput(world: int, B: int, n: int, ms_step: float) -> float:
@@ -196,7 +211,7 @@ def run_reference(args, w):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / len(vals), "higher_is_better": True,
         "scaling": "strong" if world > 1 and args.shard == "patches" else "weak",
-        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+        "vs_baseline": None, "dtype": dtype_label(w), "data": "synthetic",
         "config": workload_config(args.workload, w, world, args.shard),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "physical_cores": hc["physical_cores"], "sample": sample},
@@ -426,7 +441,7 @@ def run_gpu(args, w):
     m, B = w["m"], w["B"]
     n = 2 ** m
     cfg = _solver_cfg(fm, w)
-    plan = fm.get_plan(fm.key_from_config(cfg, B, dtype))
+    plan = fm.get_plan(fm.key_from_config(cfg, B, dtype, arith=_arith(w)))
     f = _forcing(fm, w, dtype, rank_seed(rank))
     sol = torch.empty_like(f)
     stream = torch.cuda.current_stream()
@@ -448,11 +463,14 @@ def run_gpu(args, w):
     roof = _finest_roofline(plan, cfg, w, f, sol, args.steps, ms_step, dtype, args.workload)
 
     # ---- functional-only output: u_m never stored --------------------
-    jout = torch.empty(B, dtype=dtype, device="cuda")
-    for _ in range(2):
-        plan.solve_functional(f, out=jout)
-    torch.cuda.synchronize()
-    fun_ms = _timed(lambda: plan.solve_functional(f, out=jout), args.steps, world, stream, barrier)
+    fun_ms = None  # (not offered with fp64 arithmetic on fp32 fields)
+    if _arith(w) is None:
+        jout = torch.empty(B, dtype=dtype, device="cuda")
+        for _ in range(2):
+            plan.solve_functional(f, out=jout)
+        torch.cuda.synchronize()
+        fun_ms = _timed(lambda: plan.solve_functional(f, out=jout), args.steps, world, stream,
+                        barrier)
 
     # ---- end to end through the public API with host buffers ----------------------
     # fmgsr_plan_solve_host: pinned host forcing in, pinned host solution out;
@@ -464,7 +482,7 @@ def run_gpu(args, w):
     del sol
     chunks = args.e2e_chunks or w.get("e2e_chunks", 4)
     chunks = chunks if B % chunks == 0 else 1
-    cplan = fm.get_plan(fm.key_from_config(cfg, B // chunks, dtype))
+    cplan = fm.get_plan(fm.key_from_config(cfg, B // chunks, dtype, arith=_arith(w)))
 
     def e2e_step():  # consecutive batches stream: host inputs are ready at call time
         cplan.solve_host(hf, hs, chunks, inputs_ready=True)
@@ -514,7 +532,7 @@ def run_gpu(args, w):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": w["dtype"],
+            "dtype": dtype_label(w),
             "data": ("synthetic (seeded manufactured nonlinear RHS, s ~ U[0.5, 2])"
                      if w.get("nonlinear") else "synthetic (seeded Fourier RHS, SURVEY 8(d))"),
             "config": workload_config(args.workload, w, world, "rhs"),
@@ -527,11 +545,12 @@ def run_gpu(args, w):
             "gpu_launches": info["launches_per_solve"] * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
-            "functional_only": {
+        }
+        if fun_ms is not None:
+            line["functional_only"] = {
                 "value": throughput(world, B, n, fun_ms), "unit": UNIT, "ms_per_step": fun_ms,
                 "api": "fmgsr_plan_solve_functional (J_r = h sum_i u_i per RHS; the finest "
-                       "solution is never stored)"},
-        }
+                       "solution is never stored)"}
         if extra:
             line["config2"] = extra
         print(json.dumps(line), flush=True)
@@ -613,7 +632,7 @@ def run_gpu_sharded(args, w):
     control = None
     if not args.no_extra:
         try:
-            p1 = fm.get_plan(fm.key_from_config(cfg, B, dtype))
+            p1 = fm.get_plan(fm.key_from_config(cfg, B, dtype, arith=_arith(w)))
             f1 = _forcing(fm, w, dtype, rank_seed(rank))
             s1 = torch.empty_like(f1)
             for _ in range(args.warmup):
@@ -631,7 +650,7 @@ def run_gpu_sharded(args, w):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": w["dtype"], "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
+            "dtype": dtype_label(w), "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
             "config": workload_config(args.workload, w, world, "patches"),
             "roofline": {"bound": "hbm", "achieved": alg / world / (ms_step / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s",

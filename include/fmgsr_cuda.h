@@ -213,7 +213,7 @@ typedef struct fmgsr_plan_desc {
   int32_t n_sr;       /* segmental-refinement depth, 0 <= n_sr <= m-m0-1 */
   int32_t ns;         /* inner sweeps: V(ns,ns) */
   int32_t geom_mode;  /* 0 = reference halo (W=2,b), 1 = global, 2 = P patches */
-  int32_t dtype;      /* 0 = f64, 1 = f32 */
+  int32_t dtype;      /* 0 = f64, 1 = f32, 2 = f32 fields with f64 arithmetic */
   int64_t P;          /* patches on the finest level (geom_mode 2) */
   int64_t b;          /* buffer / halo cells */
   int64_t B;          /* right-hand sides per solve */

@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <tuple>
+#include <type_traits>
 #include <string>
 #include <utility>
 #include <vector>
@@ -207,7 +208,27 @@ struct Plan : PlanBase {
   }
 #define FMGSR_PLAN_FWD(NAME) \
   template <class... A> void NAME(A&&... a) { if (!dry) fmgsr::NAME(std::forward<A>(a)...); }
-  FMGSR_PLAN_FWD(launch_visit)
+  // fp32 fields with fp64 arithmetic (dtype 2, T = float): every kernel
+  // widens on load, computes in fp64 and rounds once per stored value; edge
+  // records and the on-chip coarse levels are fp64
+  bool mixed = false;
+  size_t esz() const { return mixed ? sizeof(double) : sizeof(T); }  // arithmetic element
+  void launch_visit(VisitDesc<T> v, cudaStream_t s) {
+    if (dry) return;
+    v.f64_arith = mixed;
+    fmgsr::launch_visit(v, s);
+  }
+  void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, int B,
+                      cudaStream_t s) {
+    if (dry) return;
+    if constexpr (std::is_same<T, float>::value) {
+      if (mixed) {
+        launch_cascade_f64arith(src, n_src, dst, ld, B, s);
+        return;
+      }
+    }
+    fmgsr::launch_cascade(src, n_src, dst, ld, B, s);
+  }
   FMGSR_PLAN_FWD(launch_restrict_tau)
   FMGSR_PLAN_FWD(launch_prolong_fmg)
   FMGSR_PLAN_FWD(launch_fas_correct)
@@ -215,7 +236,6 @@ struct Plan : PlanBase {
   FMGSR_PLAN_FWD(launch_direct_solve_nl)
   FMGSR_PLAN_FWD(launch_coarse)
   FMGSR_PLAN_FWD(launch_coarse_warp)
-  FMGSR_PLAN_FWD(launch_cascade)
   FMGSR_PLAN_FWD(launch_smooth_ns2)
   FMGSR_PLAN_FWD(launch_smooth_scratch)
   FMGSR_PLAN_FWD(launch_edge_fix)
@@ -261,6 +281,11 @@ struct Plan : PlanBase {
     d = desc;
     S = shards;
     srank = shard;
+    mixed = d.dtype == 2;
+    if (mixed)
+      require(d.fused && d.ns == 1 && !d.nonlinear && d.coarse != 0 && S == 1,
+              "fp64 arithmetic on fp32 fields: the fused ns = 1 linear plan with the on-chip "
+              "coarse levels, unsharded");
     const int m0 = d.m0, m = d.m;
     const i64 ld = d.ld, Bp = ((d.B + 31) / 32) * 32;
     const int nrg = (int)(Bp / 32);
@@ -287,7 +312,7 @@ struct Plan : PlanBase {
     // The CTA kernel is faster where it applies (measured: config 2 3.30 vs
     // 3.70 ms); the warp kernel carries ns = 2 and the nonlinear smoother.
     const char* ck = getenv("FMGSR_COARSE");
-    coarse_warp = (d.ns != 1 || d.nonlinear) || (ck && std::string(ck) == "warp");
+    coarse_warp = !mixed && ((d.ns != 1 || d.nonlinear) || (ck && std::string(ck) == "warp"));
     use_coarse = d.fused && d.coarse != 0 && (d.ns == 1 || d.ns == 2) && d.m - d.m0 >= 2;
     const char* tr = getenv("FMGSR_COARSE_TRACE");
     coarse_trace = (tr && tr[0] == '1') ? 1 : 0;
@@ -348,7 +373,8 @@ struct Plan : PlanBase {
       Lc = m0;
       // an on-chip SR level adds a projected-copy buffer of 2^Lc cells per column
       auto smem_at = [&](int lc) {
-        return coarse_smem_bytes<T>(m0, lc, CW, lc > m - d.n_sr ? 1 << lc : 0);
+        return mixed ? coarse_smem_bytes<double>(m0, lc, CW, lc > m - d.n_sr ? 1 << lc : 0)
+                     : coarse_smem_bytes<T>(m0, lc, CW, lc > m - d.n_sr ? 1 << lc : 0);
       };
       // the coarsest level itself must fit: fewer columns per CTA, else no coarse kernel
       while (CW > 1 && smem_at(m0) > 200 * 1024) CW /= 2;
@@ -363,15 +389,21 @@ struct Plan : PlanBase {
       // finest visits then run from shared memory too and a solve is two
       // launches (auto, or coarse = m + 1; FMGSR_COARSE_WHOLE=0 disables).
       const char* we = getenv("FMGSR_COARSE_WHOLE");
-      const bool allow = !(we && we[0] == '0');
+      const bool allow = !(we && we[0] == '0') && !mixed;
       const int nsm = devattr(cudaDevAttrMultiProcessorCount, 148);
       const bool fits = coarse_smem_bytes<T>(m0, m, CW, (m > m - d.n_sr ? 1 << m : 0) +
                                                            (1 << (m + 1)) - (1 << m0)) <= 200 * 1024 &&
                         (d.B + CW - 1) / CW <= nsm;
-      if (S == 1 && fits && ((want < 0 && allow) || want == m + 1)) {
+      if (S == 1 && !mixed && fits && ((want < 0 && allow) || want == m + 1)) {
         whole = true;
         Lc = m;
       }
+    }
+    if (mixed) {
+      require(use_coarse, "fp64 arithmetic on fp32 fields needs the on-chip coarse levels");
+      for (int l = Lc + 1; l <= m; l++)
+        require(lv[l].W >= 4, "fp64 arithmetic on fp32 fields: every level above the on-chip "
+                              "cutoff needs owned width >= 4 (the fused restriction)");
     }
     if (S > 1) {
       require(use_coarse, "sharding needs the on-chip coarse levels (coarse != 0)");
@@ -404,7 +436,7 @@ struct Plan : PlanBase {
         L.ubytes = fb;
         if (l < m) L.f = alloc(fb);
       }
-      if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * sizeof(T));
+      if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * esz());
     }
     tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
     if (!dry)
@@ -961,6 +993,7 @@ struct Plan : PlanBase {
     a.kz.recip = (T)2.0;
     a.kz.pow2 = true;
     a.trace = coarse_trace;
+    a.f64_arith = mixed ? 1 : 0;
     return a;
   }
 
@@ -1292,6 +1325,7 @@ struct Plan : PlanBase {
 
   void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) override {
     require(S == 1, "solve_functional: not available on sharded plans");
+    require(!mixed, "solve_functional: not with fp64 arithmetic on fp32 fields");
     if (!fun_part) {  // before any capture: [P_m][Bp] partial sums
       const Level& L = lv[d.m];
       fun_part = alloc((size_t)(L.n / L.W) * (((d.B + 31) / 32) * 32) * sizeof(T));
@@ -1567,7 +1601,8 @@ static void validate_desc(const fmgsr_plan_desc& d) {
   require(d.geom_mode != 2 || (d.P >= 1 && is_pow2(d.P)), "P must be a power of two");
   require(d.b >= 0, "buffer must be >= 0");
   require(d.B >= 1 && d.ld >= d.B, "need 1 <= B <= ld");
-  require(d.dtype == 0 || d.dtype == 1, "dtype must be 0 (f64) or 1 (f32)");
+  require(d.dtype >= 0 && d.dtype <= 2,
+          "dtype must be 0 (f64), 1 (f32) or 2 (f32 fields, f64 arithmetic)");
   require(((i64)1 << d.m0) <= 2048, "coarsest level above 2048 cells");
   require(!d.nonlinear || ((i64)1 << d.m0) <= 64, "nonlinear: coarsest level above 64 cells");
 }

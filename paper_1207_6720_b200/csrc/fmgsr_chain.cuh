@@ -24,21 +24,22 @@
 
 namespace fmgsr {
 
+// M: the fields' storage type (T, or fp32 under fp64 arithmetic T)
 template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, int NT, int D, bool BULK,
-          bool FUNC = false>
+          bool FUNC = false, typename M = T>
 struct Chain {
   static constexpr int R = SrcRows<SRC, CR>::R;
-  PairSource<T, SRC, CR> src;
+  PairSource<T, SRC, CR, M> src;
   GsCoef<T> gc;
   i64 n, nc, ld, ws, os, oe;
-  T* out;  // u_l output, column-offset (nullptr: not written)
+  M* out;  // u_l output, column-offset (nullptr: not written)
   // FUNC: instead of writing the owned cells, accumulate sum_i w_i u_i over
   // them in cell order (w column-offset; nullptr: unit weights)
-  const T* fw;
+  const M* fw;
   T facc;
   bool store;
-  T* ring;  // this lane's ring: slot s, row k at ring[(s * R + k) * NT]
-  Epilogue<T>* epi;
+  M* ring;  // this lane's ring: slot s, row k at ring[(s * R + k) * NT]
+  Epilogue<T, M>* epi;
   // BULK staging: the warp's D mbarriers; pair x lives in slot x & (D-1) and
   // completes phase ((x - x0) / D) & 1 of that slot's barrier
   unsigned long long* bars;
@@ -47,7 +48,7 @@ struct Chain {
   // chain state: uL = new value left of the current pair; (v0, v1, f0, f1) = current pair
   T uL, v0, v1, f0, f1;
 
-  __device__ __forceinline__ T* slot(i64 x) const { return ring + (i64)((x & (D - 1)) * R) * NT; }
+  __device__ __forceinline__ M* slot(i64 x) const { return ring + (i64)((x & (D - 1)) * R) * NT; }
 
   // stage pair g into slot(g): per-lane cp.async, or one bulk copy per row
   __device__ __forceinline__ void stage(i64 g) {
@@ -58,14 +59,14 @@ struct Chain {
     }
     __syncwarp();  // every lane is done reading this slot's previous pair
     if (lane == 0) {
-      const T* p[R];
+      const M* p[R];
       src.rows(g, 0, p);
       unsigned long long* bar = bars + (g & (D - 1));
-      T* dst = slot(g);  // lane 0: the warp's 32-column segment of each row
+      M* dst = slot(g);  // lane 0: the warp's 32-column segment of each row
       if (FMGSR_PROXY_FENCE) fence_proxy_async();
-      mbar_expect_tx(bar, R * 32 * sizeof(T));
+      mbar_expect_tx(bar, R * 32 * sizeof(M));
 #pragma unroll
-      for (int k = 0; k < R; k++) bulk_g2s(dst + k * NT, p[k], 32 * sizeof(T), bar);
+      for (int k = 0; k < R; k++) bulk_g2s(dst + k * NT, p[k], 32 * sizeof(M), bar);
     }
   }
   // wait until pair g has landed in its slot; AHEAD = g - (the pair whose
@@ -110,17 +111,17 @@ struct Chain {
     if (EPI) {
       if (i0 >= os) {  // owned pairs are whole pairs (os, oe even)
         if (out && store) {
-          out[i0 * ld] = n0;
-          out[i1 * ld] = n1;
+          out[i0 * ld] = cvt<M>(n0);
+          out[i1 * ld] = cvt<M>(n1);
         }
         epi->push(q, n0, n1, f0, f1, store);
       }
     } else if (FUNC) {
-      if (i0 >= os && i0 < oe) facc = xadd(facc, fw ? xmul(fw[i0 * ld], n0) : n0);
-      if (i1 >= os && i1 < oe) facc = xadd(facc, fw ? xmul(fw[i1 * ld], n1) : n1);
+      if (i0 >= os && i0 < oe) facc = xadd(facc, fw ? xmul(cvt<T>(fw[i0 * ld]), n0) : n0);
+      if (i1 >= os && i1 < oe) facc = xadd(facc, fw ? xmul(cvt<T>(fw[i1 * ld]), n1) : n1);
     } else if (store) {
-      if (i0 >= os && i0 < oe) out[i0 * ld] = n0;
-      if (i1 >= os && i1 < oe) out[i1 * ld] = n1;
+      if (i0 >= os && i0 < oe) out[i0 * ld] = cvt<M>(n0);
+      if (i1 >= os && i1 < oe) out[i1 * ld] = cvt<M>(n1);
     }
     v0 = w0;
     v1 = w1;
@@ -215,21 +216,21 @@ struct Chain {
   __device__ __forceinline__ void run_fast(i64 q, i64 q_end) {
     if (q > q_end) return;
     if (!BULK) src.fast_ptrs(q + D);
-    T* po = (OWNED && WU) ? out + (2 * q) * ld : nullptr;
-    const T* pw = (FUNC && OWNED && fw) ? fw + (2 * q) * ld : nullptr;
+    M* po = (OWNED && WU) ? out + (2 * q) * ld : nullptr;
+    const M* pw = (FUNC && OWNED && fw) ? fw + (2 * q) * ld : nullptr;
     auto emit = [&](T n0, T n1) {
       if (FUNC && OWNED) {
         if (pw) {
-          facc = xadd(facc, xmul(pw[0], n0));
-          facc = xadd(facc, xmul(pw[ld], n1));
+          facc = xadd(facc, xmul(cvt<T>(pw[0]), n0));
+          facc = xadd(facc, xmul(cvt<T>(pw[ld]), n1));
           pw += 2 * ld;
         } else {
           facc = xadd(facc, n0);
           facc = xadd(facc, n1);
         }
       } else if (OWNED && WU) {
-        po[0] = n0;
-        po[ld] = n1;
+        po[0] = cvt<M>(n0);
+        po[ld] = cvt<M>(n1);
         po += 2 * ld;
       }
     };
@@ -334,17 +335,17 @@ struct Chain {
   __device__ __forceinline__ void run(i64 we) {
     const i64 qs = (ws > 0) ? ((ws - 1) >> 1) : 0;
     const i64 qe = (oe - 1) >> 1;
-    // chain head: the D-1 staged pairs are issued first so their latency
-    // overlaps the direct loads of the state before pair qs and of pair qs
+    // chain head: the direct loads of the state before pair qs and of pair qs
+    // gate the chain, so they are issued first; the D-1 staged pairs follow
+    // while they are in flight (one memory latency for the whole head)
     x0 = qs + 1;
+    src.init_loads(qs);
+    Raw<T> r0 = src.load(qs);
     for (int k = 1; k < D; k++) stage(qs + k);
-    src.init(qs);
-    {
-      Raw<T> r = src.load(qs);
-      src.make(qs, r, v0, v1);
-      f0 = r.f0;
-      f1 = r.f1;
-    }
+    src.init_finish(qs);
+    src.make(qs, r0, v0, v1);
+    f0 = r0.f0;
+    f1 = r0.f1;
     uL = T(0);
     // interior range: both cells updated and interior, generation of q+1
     // interior, CR window interior, unclamped fast issue of q + D

@@ -77,6 +77,27 @@ struct LaneCols<V2<S>> {
   static constexpr int value = 2;
 };
 
+// Storage <-> arithmetic conversions.  Fields may be stored narrower than the
+// arithmetic type (fp32 storage, fp64 arithmetic: values widen exactly on
+// load and round to nearest once on store).
+template <typename To>
+__device__ __forceinline__ To cvt(double x);
+template <typename To>
+__device__ __forceinline__ To cvt(float x);
+template <>
+__device__ __forceinline__ double cvt<double>(double x) { return x; }
+template <>
+__device__ __forceinline__ float cvt<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ double cvt<double>(float x) { return (double)x; }
+template <>
+__device__ __forceinline__ float cvt<float>(double x) { return __double2float_rn(x); }
+template <typename To, typename S>
+__device__ __forceinline__ To cvt(V2<S> x) {
+  using E = decltype(To::x);
+  return To(cvt<E>(x.x), cvt<E>(x.y));
+}
+
 // ---------------------------------------------------------------------------
 // Gauss-Seidel cell updates, reference _kernels_numba.py:26-35.
 //   interior : resid = f - inv_h2*((2u - uL) - uR), u += (omega*resid)/(2 inv_h2)
@@ -312,13 +333,15 @@ struct SrcRows {
       2 + (SRC == SRC_LOAD ? 2 : SRC == SRC_CORR ? 3 : 1) + ((CR && SRC != SRC_FMG) ? 1 : 0);
 };
 
-template <typename T, int SRC, bool CR>
+template <typename T, int SRC, bool CR, typename M = T>
 struct PairSource {
   static constexpr int R = SrcRows<SRC, CR>::R;
-  const T* u;   // fine field, column-offset (LOAD, CORR)
-  const T* uH;  // coarse field (CORR, FMG; CR target for FMG)
-  const T* uc;  // CR target for LOAD / CORR
-  const T* f;   // level right-hand side
+  // fields are stored as M (= T, or fp32 under fp64 arithmetic); the ring
+  // stages them unconverted, fetch()/load()/init() widen to T
+  const M* u;   // fine field, column-offset (LOAD, CORR)
+  const M* uH;  // coarse field (CORR, FMG; CR target for FMG)
+  const M* uc;  // CR target for LOAD / CORR
+  const M* f;   // level right-hand side
   i64 ld, nc;   // row stride, number of pairs (= coarse cells)
   KzCoef<T> kz;
   i64 wlo, whi;  // Kaczmarz pair range
@@ -326,13 +349,13 @@ struct PairSource {
   T s0, s1, s2, s3;
   // fast-issue row pointers (pair g): f row 2g, u row (LOAD 2g | CORR 2g+2),
   // uH row (CORR g+1 | FMG g+2), uc row g
-  const T *pf, *pu, *ph, *pc;
+  const M *pf, *pu, *ph, *pc;
 
   __device__ __forceinline__ i64 cl(i64 q) const { return q < qlo ? qlo : (q > qhi ? qhi : q); }
 
   // slot layout: sl[k * NT] for k < R (NT = threads per block)
   template <int NT>
-  __device__ __forceinline__ void issue(T* sl, i64 g) const {
+  __device__ __forceinline__ void issue(M* sl, i64 g) const {
     i64 gg = cl(g);
     cp_async(sl, f + (2 * gg) * ld);
     cp_async(sl + NT, f + (2 * gg + 1) * ld);
@@ -352,7 +375,7 @@ struct PairSource {
 
   // the R source rows of pair g (clamped), per-lane pointers shifted by -off
   // (off = lane gives the warp's 32-column row segment for a bulk copy)
-  __device__ __forceinline__ void rows(i64 g, int off, const T* (&p)[R]) const {
+  __device__ __forceinline__ void rows(i64 g, int off, const M* (&p)[R]) const {
     i64 gg = cl(g);
     p[0] = f + (2 * gg) * ld - off;
     p[1] = f + (2 * gg + 1) * ld - off;
@@ -383,7 +406,7 @@ struct PairSource {
 
   // unclamped issue of the pair at the fast pointers, then advance one pair
   template <int NT>
-  __device__ __forceinline__ void issue_fast(T* sl) {
+  __device__ __forceinline__ void issue_fast(M* sl) {
     cp_async(sl, pf);
     cp_async(sl + NT, pf + ld);
     pf += 2 * ld;
@@ -408,22 +431,22 @@ struct PairSource {
   }
 
   template <int NT>
-  __device__ __forceinline__ Raw<T> fetch(const T* sl) const {
+  __device__ __forceinline__ Raw<T> fetch(const M* sl) const {
     Raw<T> r;
-    r.f0 = sl[0];
-    r.f1 = sl[NT];
+    r.f0 = cvt<T>(sl[0]);
+    r.f1 = cvt<T>(sl[NT]);
     r.a0 = r.a1 = r.h = r.g = T(0);
     if (SRC == SRC_LOAD) {
-      r.a0 = sl[2 * NT];
-      r.a1 = sl[3 * NT];
+      r.a0 = cvt<T>(sl[2 * NT]);
+      r.a1 = cvt<T>(sl[3 * NT]);
     } else if (SRC == SRC_CORR) {
-      r.a0 = sl[2 * NT];
-      r.a1 = sl[3 * NT];
-      r.h = sl[4 * NT];
+      r.a0 = cvt<T>(sl[2 * NT]);
+      r.a1 = cvt<T>(sl[3 * NT]);
+      r.h = cvt<T>(sl[4 * NT]);
     } else {
-      r.h = sl[2 * NT];
+      r.h = cvt<T>(sl[2 * NT]);
     }
-    if (CR && SRC != SRC_FMG) r.g = sl[(R - 1) * NT];
+    if (CR && SRC != SRC_FMG) r.g = cvt<T>(sl[(R - 1) * NT]);
     return r;
   }
 
@@ -431,44 +454,63 @@ struct PairSource {
   __device__ __forceinline__ Raw<T> load(i64 q) const {
     Raw<T> r;
     i64 qq = cl(q);
-    r.f0 = f[(2 * qq) * ld];
-    r.f1 = f[(2 * qq + 1) * ld];
+    r.f0 = cvt<T>(f[(2 * qq) * ld]);
+    r.f1 = cvt<T>(f[(2 * qq + 1) * ld]);
     r.a0 = r.a1 = r.h = r.g = T(0);
     if (SRC == SRC_LOAD) {
-      r.a0 = u[(2 * qq) * ld];
-      r.a1 = u[(2 * qq + 1) * ld];
+      r.a0 = cvt<T>(u[(2 * qq) * ld]);
+      r.a1 = cvt<T>(u[(2 * qq + 1) * ld]);
     } else if (SRC == SRC_CORR) {
       i64 q1 = cl(q + 1);
-      r.a0 = u[(2 * q1) * ld];
-      r.a1 = u[(2 * q1 + 1) * ld];
-      r.h = uH[q1 * ld];
+      r.a0 = cvt<T>(u[(2 * q1) * ld]);
+      r.a1 = cvt<T>(u[(2 * q1 + 1) * ld]);
+      r.h = cvt<T>(uH[q1 * ld]);
     } else {
-      r.h = uH[cl(q + 2) * ld];
+      r.h = cvt<T>(uH[cl(q + 2) * ld]);
     }
-    if (CR && SRC != SRC_FMG) r.g = uc[qq * ld];
+    if (CR && SRC != SRC_FMG) r.g = cvt<T>(uc[qq * ld]);
     return r;
   }
 
-  // sliding-window state before make(q)
-  __device__ __forceinline__ void init(i64 q) {
+  // sliding-window state before make(q), in two halves so that a chain head
+  // can issue these loads before it stages its ring (the cp.async asm is a
+  // compiler memory barrier: loads written after it are issued after it)
+  T h0, h1, h2, h3, h4, h5;  // raw head values (init_loads -> init_finish)
+  __device__ __forceinline__ void init_loads(i64 q) {
     if (SRC == SRC_CORR) {
-      // s0 = c_{q-1}, s1 = c_q, s2 = u[2q], s3 = u[2q+1]; c_j = uH[j] - 0.5(u[2j] + u[2j+1])
-      s2 = u[(2 * q) * ld];
-      s3 = u[(2 * q + 1) * ld];
-      s1 = xsub(uH[q * ld], xmul(T(0.5), xadd(s2, s3)));
+      h2 = cvt<T>(u[(2 * q) * ld]);
+      h3 = cvt<T>(u[(2 * q + 1) * ld]);
+      h1 = cvt<T>(uH[q * ld]);
       if (q >= 1) {
-        T a = u[(2 * q - 2) * ld], b = u[(2 * q - 1) * ld];
-        s0 = xsub(uH[(q - 1) * ld], xmul(T(0.5), xadd(a, b)));
-      } else {
-        s0 = T(0);
+        h4 = cvt<T>(u[(2 * q - 2) * ld]);
+        h5 = cvt<T>(u[(2 * q - 1) * ld]);
+        h0 = cvt<T>(uH[(q - 1) * ld]);
       }
     } else if (SRC == SRC_FMG) {
-      // s0..s3 = c[q-2], c[q-1], c[q], c[q+1] (clamped; boundary rows ignore them)
-      s0 = uH[cl(q - 2) * ld];
-      s1 = uH[cl(q - 1) * ld];
-      s2 = uH[cl(q) * ld];
-      s3 = uH[cl(q + 1) * ld];
+      h0 = cvt<T>(uH[cl(q - 2) * ld]);
+      h1 = cvt<T>(uH[cl(q - 1) * ld]);
+      h2 = cvt<T>(uH[cl(q) * ld]);
+      h3 = cvt<T>(uH[cl(q + 1) * ld]);
     }
+  }
+  __device__ __forceinline__ void init_finish(i64 q) {
+    if (SRC == SRC_CORR) {
+      // s0 = c_{q-1}, s1 = c_q, s2 = u[2q], s3 = u[2q+1]; c_j = uH[j] - 0.5(u[2j] + u[2j+1])
+      s2 = h2;
+      s3 = h3;
+      s1 = xsub(h1, xmul(T(0.5), xadd(s2, s3)));
+      s0 = q >= 1 ? xsub(h0, xmul(T(0.5), xadd(h4, h5))) : T(0);
+    } else if (SRC == SRC_FMG) {
+      // s0..s3 = c[q-2], c[q-1], c[q], c[q+1] (clamped; boundary rows ignore them)
+      s0 = h0;
+      s1 = h1;
+      s2 = h2;
+      s3 = h3;
+    }
+  }
+  __device__ __forceinline__ void init(i64 q) {
+    init_loads(q);
+    init_finish(q);
   }
 
   // interior FMG rows (stencils.py:90-97), then /128 as an exact scaling
@@ -571,12 +613,12 @@ struct EdgeRec {
   T v[5];
 };
 
-template <typename T>
+template <typename T, typename M = T>
 struct Epilogue {
   T inv_h2, inv_H2;
   bool left_dom, right_dom, write_uH;
-  T* uH_out;  // column-offset
-  T* fH_out;  // column-offset
+  M* uH_out;  // column-offset (fields stored as M)
+  M* fH_out;  // column-offset
   i64 ld, nc;
   T up2, up1, Lprev, Rm2, Rm1, Rfm1;
   EdgeRec<T> left;  // u[os], u[os+1], Lu[os+1], Ru_{j0+1}, Rf_{j0}
@@ -585,7 +627,7 @@ struct Epilogue {
   __device__ __forceinline__ void push(i64 j, T a, T b, T f0, T f1, bool store) {
     T Rj = xmul(T(0.5), xadd(a, b));
     T Rfj = xmul(T(0.5), xadd(f0, f1));
-    if (write_uH && store) uH_out[j * ld] = Rj;
+    if (write_uH && store) uH_out[j * ld] = cvt<M>(Rj);
     if (cnt == 0) {
       if (left_dom) {
         Lprev = xmul(xsub(xmul(T(3), a), b), inv_h2);  // Lu[0]
@@ -603,7 +645,7 @@ struct Epilogue {
         T RL = xmul(T(0.5), xadd(Lprev, Lodd));
         T LH = (j - 1 == 0) ? xmul(xsub(xmul(T(3), Rm1), Rj), inv_H2)
                             : xmul(xsub(xsub(xmul(T(2), Rm1), Rm2), Rj), inv_H2);
-        if (store) fH_out[(j - 1) * ld] = xadd(Rfm1, xsub(LH, RL));
+        if (store) fH_out[(j - 1) * ld] = cvt<M>(xadd(Rfm1, xsub(LH, RL)));
       }
       Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);  // Lu[2j]
     }
@@ -617,8 +659,8 @@ struct Epilogue {
 
   // steady-state push (cnt >= 2, coarse cell j-1 interior): pointer-walking
   // version of push() for the chain's fast loop; call fast_begin(j) first.
-  T* puH;
-  T* pfH;
+  M* puH;
+  M* pfH;
   __device__ __forceinline__ void fast_begin(i64 j) {
     puH = uH_out ? uH_out + j * ld : nullptr;
     pfH = fH_out + (j - 1) * ld;
@@ -629,13 +671,13 @@ struct Epilogue {
     T Rj = xmul(T(0.5), xadd(a, b));
     T Rfj = xmul(T(0.5), xadd(f0, f1));
     if (WUH) {
-      *puH = Rj;
+      *puH = cvt<M>(Rj);
       puH += ld;
     }
     T Lodd = xmul(xsub(xsub(xmul(T(2), up1), up2), a), inv_h2);
     T RL = xmul(T(0.5), xadd(Lprev, Lodd));
     T LH = xmul(xsub(xsub(xmul(T(2), Rm1), Rm2), Rj), inv_H2);
-    *pfH = xadd(Rfm1, xsub(LH, RL));
+    *pfH = cvt<M>(xadd(Rfm1, xsub(LH, RL)));
     pfH += ld;
     Lprev = xmul(xsub(xsub(xmul(T(2), a), up1), b), inv_h2);
     up2 = a;
@@ -652,7 +694,7 @@ struct Epilogue {
       T Llast = xmul(xsub(xmul(T(3), up1), up2), inv_h2);  // Lu[n-1]
       T RL = xmul(T(0.5), xadd(Lprev, Llast));
       T LH = xmul(xsub(xmul(T(3), Rm1), Rm2), inv_H2);
-      if (store) fH_out[(nc - 1) * ld] = xadd(Rfm1, xsub(LH, RL));
+      if (store) fH_out[(nc - 1) * ld] = cvt<M>(xadd(Rfm1, xsub(LH, RL)));
     } else {
       right.v[0] = up2;    // u[s-2]
       right.v[1] = up1;    // u[s-1]
@@ -702,10 +744,10 @@ __device__ __forceinline__ void edge_finish(const T* L, const T* R, T inv_h2, T 
 // boundary's counter; the warp that sees an odd old value arrived second and
 // finishes both coarse cells.  Every boundary receives exactly two arrivals
 // per visit, so the parity test stays valid across visits without resets.
-template <typename T, bool NL = false>
+template <typename T, bool NL = false, typename M = T>
 __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i64 bi, int side,
                                             const EdgeRec<T>& rec, int lane, int rg, int r,
-                                            bool store, T* fH, i64 ld, i64 s, T inv_h2,
+                                            bool store, M* fH, i64 ld, i64 s, T inv_h2,
                                             T inv_H2) {
   T* mine = E + (bi * 10 + side * 5) * ldE + r;
 #pragma unroll
@@ -727,8 +769,8 @@ __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i6
     T fL, fR;
     edge_finish<T, NL>(Lr, Rr, inv_h2, inv_H2, fL, fR);
     if (store) {
-      fH[(s / 2 - 1) * ld] = fL;
-      fH[(s / 2) * ld] = fR;
+      fH[(s / 2 - 1) * ld] = cvt<M>(fL);
+      fH[(s / 2) * ld] = cvt<M>(fR);
     }
   }
 }
@@ -739,9 +781,9 @@ __device__ __forceinline__ void edge_arrive(T* E, int* cnt, i64 ldE, int nrg, i6
 // round trip fewer per warp.  doL: the left boundary (index biL = p, this warp
 // is its side 1, fine cell sL = os); doR: the right one (biR = p + 1, side 0,
 // sR = oe).
-template <typename T, bool NL = false>
+template <typename T, bool NL = false, typename M = T>
 __device__ __forceinline__ void edge_arrive2(T* E, int* cnt, i64 ldE, int nrg, int lane, int rg,
-                                             int r, bool store, T* fH, i64 ld, T inv_h2,
+                                             int r, bool store, M* fH, i64 ld, T inv_h2,
                                              T inv_H2, bool doL, i64 biL,
                                              const EdgeRec<T>& recL, i64 sL, bool doR, i64 biR,
                                              const EdgeRec<T>& recR, i64 sR) {
@@ -779,8 +821,8 @@ __device__ __forceinline__ void edge_arrive2(T* E, int* cnt, i64 ldE, int nrg, i
     T fL, fR;
     edge_finish<T, NL>(Lr, Rr, inv_h2, inv_H2, fL, fR);
     if (store) {
-      fH[(s / 2 - 1) * ld] = fL;
-      fH[(s / 2) * ld] = fR;
+      fH[(s / 2 - 1) * ld] = cvt<M>(fL);
+      fH[(s / 2) * ld] = cvt<M>(fR);
     }
   };
   if (finL) finish(biL, sL);

@@ -89,16 +89,18 @@ struct KzCoef {
 
 // Coarse hierarchy kernel (kernels_coarse.cu): one CTA per CW RHS columns
 // runs every visit of levels m0..Lc out of shared memory.
-template <typename T>
+// M: storage type of the global fields it reads and writes (forig, f_top,
+// u_top); levels on chip and all arithmetic are T.
+template <typename T, typename M = T>
 struct CoarseArgs {
   int m0 = 0, Lc = 0, m = 0, n_sr = 0;
   int mode = 0;  // 0: coarse FMG steps m0+1..Lc; 1: V-cycle segment below Lc+1
   int CW = 1, B = 1;
   i64 ld = 0;
   i64 W[32] = {}, b[32] = {};
-  const T* forig[32] = {};  // mode 0: restricted forcing per level
-  const T* f_top = nullptr;  // mode 1: f_{Lc}
-  T* u_top = nullptr;        // mode 1: in/out u_{Lc}; mode 0: out
+  const M* forig[32] = {};  // mode 0: restricted forcing per level
+  const M* f_top = nullptr;  // mode 1: f_{Lc}
+  M* u_top = nullptr;        // mode 1: in/out u_{Lc}; mode 0: out
   double omega = 1.0;
   KzCoef<T> kz{};
   int trace = 0;  // debug: per-phase clock printf from CTA 0
@@ -114,6 +116,9 @@ struct CoarseArgs {
   // memory from forig[m] (extra 2^(m+1) - 2^m0 cells per column) instead of
   // loading each restricted level from global memory
   int fo = 0;
+  // fp32 fields (T = float) with fp64 arithmetic: the CTAs keep their levels
+  // and compute in fp64, widening on load and rounding once on store
+  int f64_arith = 0;
 };
 template <typename T> void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s);
 template <typename T> size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells = 0);
@@ -129,6 +134,9 @@ struct CascadeDst {
 };
 template <typename T>
 void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, int B, cudaStream_t s);
+// fp32 fields, fp64 arithmetic: the pair averages in fp64, each level rounded once
+void launch_cascade_f64arith(const float* src, i64 n_src, const CascadeDst<float>& dst, i64 ld,
+                             int B, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // Level-visit descriptor (uniform patch geometry: owned width W, buffer b).
@@ -168,6 +176,10 @@ struct VisitDesc {
   // functional output (final up visit): partial sums instead of the field
   const T* fun_w = nullptr;
   T* fun_part = nullptr;  // [P][round_up(B, 32)]
+  // fp32 fields with fp64 arithmetic (T = float only): every value widens
+  // exactly on load, the visit computes in fp64, stores round once to fp32;
+  // E / E_out then hold fp64 records (twice the fp32 workspace)
+  bool f64_arith = false;
 };
 
 // functional J = scale * sum_p sum_{owned i} w_i u_i (w nullptr: unit weights)

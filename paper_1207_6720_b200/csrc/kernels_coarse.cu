@@ -18,8 +18,10 @@
 // (the f cascade, cycles.py:178-180).
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 
 #include "fmgsr_device.cuh"
+
 #include "fmgsr_internal.h"
 
 namespace fmgsr {
@@ -40,9 +42,9 @@ __device__ __forceinline__ T pow4(int l) {
 // 3 CW (2^l - 2^m0); a level's current u buffer is one bit of `curmask`.
 // Everything is addressed arithmetically (no per-level tables), so nothing
 // spills to local memory.
-template <typename T, int CW>
+template <typename T, int CW, typename M = T>
 struct CoarseCtx {
-  const CoarseArgs<T>& a;
+  const CoarseArgs<T, M>& a;
   T* sm;
   const T* dfac;  // direct-solve factor d[n0], e[n0], RN(1/d)[n0]
   const T* efac;
@@ -70,7 +72,7 @@ struct CoarseCtx {
   }
   int c0;
   unsigned curmask;
-  __device__ CoarseCtx(const CoarseArgs<T>& args) : a(args) {}
+  __device__ CoarseCtx(const CoarseArgs<T, M>& args) : a(args) {}
 
   __device__ __forceinline__ int nlev(int l) const { return 1 << l; }
   __device__ __forceinline__ T* U(int l, int w) const {
@@ -113,19 +115,24 @@ struct CoarseCtx {
   }
 
   // global -> shared by cp.async: every element in flight at once, one wait
-  __device__ void load(T* dst, const T* src, int n) {
+  // (narrower storage: plain loads, widened exactly)
+  __device__ void load(T* dst, const M* src, int n) {
     for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
       int i = e / CW, c = e % CW, col = c0 + c;
-      if (col < a.B) cp_async(dst + e, src + (i64)i * a.ld + col);
-      else dst[e] = T(0);
+      if (col < a.B) {
+        if constexpr (std::is_same<T, M>::value) cp_async(dst + e, src + (i64)i * a.ld + col);
+        else dst[e] = cvt<T>(src[(i64)i * a.ld + col]);
+      } else {
+        dst[e] = T(0);
+      }
     }
     cp_commit();
     cp_wait<0>();
   }
-  __device__ void store(T* dst, const T* src, int n) {
+  __device__ void store(M* dst, const T* src, int n) {
     for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
       int i = e / CW, c = e % CW, col = c0 + c;
-      if (col < a.B) dst[(i64)i * a.ld + col] = src[e];
+      if (col < a.B) dst[(i64)i * a.ld + col] = cvt<M>(src[e]);
     }
   }
 
@@ -370,10 +377,10 @@ struct CoarseCtx {
   }
 };
 
-template <typename T, int CW>
-__global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
+template <typename T, int CW, typename M = T>
+__global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T, M> a) {
   extern __shared__ __align__(16) unsigned char coarse_smem[];
-  CoarseCtx<T, CW> x(a);
+  CoarseCtx<T, CW, M> x(a);
   x.sm = reinterpret_cast<T*>(coarse_smem);
   x.c0 = blockIdx.x * CW;
   x.curmask = 0;
@@ -435,18 +442,18 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T> a) {
 // f cascade: each thread restricts 2^S consecutive rows of one column down S
 // levels with a binary-counter stack, pairing (left, right) exactly like
 // restrict() applied level by level (stencils.py:39-47).
-template <typename T, int S>
-__global__ void k_cascade(const T* __restrict__ src, CascadeDst<T> dst, i64 n_src, i64 ld, int B) {
+template <typename T, int S, typename M = T>
+__global__ void k_cascade(const M* __restrict__ src, CascadeDst<M> dst, i64 n_src, i64 ld, int B) {
   int r = blockIdx.x * 32 + threadIdx.x;
   if (r >= B) return;
   const i64 nblk = n_src >> S;
   for (i64 blk = (i64)blockIdx.y * blockDim.y + threadIdx.y; blk < nblk;
        blk += (i64)gridDim.y * blockDim.y) {
-    const T* s = src + (blk << S) * ld + r;
+    const M* s = src + (blk << S) * ld + r;
     T stack[S];
 #pragma unroll
     for (int i = 0; i < (1 << S); i++) {
-      T v = s[(i64)i * ld];
+      T v = cvt<T>(s[(i64)i * ld]);
 #pragma unroll
       for (int k = 0; k < S; k++) {
         // at step i, level k+1 completes iff the low k+1 bits of i are all ones
@@ -456,7 +463,7 @@ __global__ void k_cascade(const T* __restrict__ src, CascadeDst<T> dst, i64 n_sr
         }
         v = xmul(T(0.5), xadd(stack[k], v));
         i64 idx = ((blk << S) + i) >> (k + 1);
-        dst.p[k][idx * ld + r] = v;
+        dst.p[k][idx * ld + r] = cvt<M>(v);
       }
     }
   }
@@ -471,16 +478,16 @@ size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells) {
   return (size_t)(3 * cells * CW + 3 * ((i64)1 << m0) + (i64)extra_cells * CW) * sizeof(T);
 }
 
-template <typename T, int CW>
-static void launch_coarse_cw(const CoarseArgs<T>& a, size_t smem, cudaStream_t s) {
-  const int granted = smem_optin((const void*)coarse_kernel<T, CW>);
+template <typename T, int CW, typename M>
+static void launch_coarse_cw(const CoarseArgs<T, M>& a, size_t smem, cudaStream_t s) {
+  const int granted = smem_optin((const void*)coarse_kernel<T, CW, M>);
   require(smem <= (size_t)granted, "coarse: shared memory budget exceeded");
   unsigned blocks = (unsigned)((a.B + CW - 1) / CW);
-  coarse_kernel<T, CW><<<blocks, CNT, smem, s>>>(a);
+  coarse_kernel<T, CW, M><<<blocks, CNT, smem, s>>>(a);
 }
 
-template <typename T>
-void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
+template <typename T, typename M>
+static void launch_coarse_tm(const CoarseArgs<T, M>& a, cudaStream_t s) {
   require(a.Lc >= a.m0 && a.Lc < 31, "coarse: bad cutoff");
   size_t smem = coarse_smem_bytes<T>(a.m0, a.Lc, a.CW,
                                      (a.pj ? 1 << a.Lc : 0) +
@@ -500,6 +507,37 @@ void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
 }
 
 template <typename T>
+void launch_coarse(const CoarseArgs<T>& a, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (a.f64_arith) {  // fp64 levels on chip over the fp32 fields
+      CoarseArgs<double, float> b;
+      b.m0 = a.m0, b.Lc = a.Lc, b.m = a.m, b.n_sr = a.n_sr, b.mode = a.mode;
+      b.CW = a.CW, b.B = a.B, b.ld = a.ld;
+      for (int l = 0; l < 32; l++) {
+        b.W[l] = a.W[l];
+        b.b[l] = a.b[l];
+        b.forig[l] = a.forig[l];
+        b.lgW[l] = a.lgW[l];
+        b.off[l] = a.off[l];
+        b.slen[l] = a.slen[l];
+      }
+      b.f_top = a.f_top;
+      b.u_top = a.u_top;
+      b.omega = a.omega;
+      b.kz.proj_diag = (double)a.kz.proj_diag;
+      b.kz.recip = (double)a.kz.recip;
+      b.kz.pow2 = a.kz.pow2;
+      b.trace = a.trace;
+      b.fields = a.fields, b.scratch = a.scratch, b.nw = a.nw, b.pj = a.pj, b.fo = a.fo;
+      require(!b.fo, "coarse: fp64 arithmetic on fp32 fields needs the f cascade in HBM");
+      launch_coarse_tm(b, s);
+      return;
+    }
+  }
+  launch_coarse_tm(a, s);
+}
+
+template <typename T>
 void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, int B,
                     cudaStream_t s) {
   require(dst.levels >= 1 && dst.levels <= 6, "cascade: 1..6 levels per launch");
@@ -515,6 +553,25 @@ void launch_cascade(const T* src, i64 n_src, const CascadeDst<T>& dst, i64 ld, i
     case 4: k_cascade<T, 4><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
     case 5: k_cascade<T, 5><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
     default: k_cascade<T, 6><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+  }
+  check_launch("cascade");
+}
+
+void launch_cascade_f64arith(const float* src, i64 n_src, const CascadeDst<float>& dst, i64 ld,
+                             int B, cudaStream_t s) {
+  require(dst.levels >= 1 && dst.levels <= 6, "cascade: 1..6 levels per launch");
+  require((n_src >> dst.levels) >= 1, "cascade: too many levels");
+  dim3 block(32, 4);
+  i64 blocks_y = ((n_src >> dst.levels) + 3) / 4;
+  if (blocks_y > 16384) blocks_y = 16384;
+  dim3 grid((unsigned)((B + 31) / 32), (unsigned)blocks_y);
+  switch (dst.levels) {
+    case 1: k_cascade<double, 1, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 2: k_cascade<double, 2, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 3: k_cascade<double, 3, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 4: k_cascade<double, 4, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    case 5: k_cascade<double, 5, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
+    default: k_cascade<double, 6, float><<<grid, block, 0, s>>>(src, dst, n_src, ld, B); break;
   }
   check_launch("cascade");
 }

@@ -60,8 +60,23 @@ static bool visit_few_chains(const VisitDesc<T>& d) {
 
 // the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
 // compiled in parallel)
-template <typename TV, typename T, int SHAPE>
+template <typename TV, typename T, int SHAPE, typename TM = TV>
 void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s);
+
+// fp32 fields, fp64 arithmetic (kernels_visit_m{d,v2d}.cu); only T = float
+template <typename T>
+static void visit_launch_mixed(const VisitDesc<T>& d, bool v2, bool few, cudaStream_t s) {
+  (void)d, (void)v2, (void)few, (void)s;
+  require(false, "visit: fp64 arithmetic applies to fp32 fields only");
+}
+template <>
+void visit_launch_mixed<float>(const VisitDesc<float>& d, bool v2, bool few, cudaStream_t s) {
+  require(((uintptr_t)d.E & 15) == 0 && ((uintptr_t)d.E_out & 15) == 0,
+          "visit: fp64 edge records must be 16-byte aligned");
+  if (v2) visit_fill_launch<V2<double>, float, SHAPE_WIDE, V2<float>>(d, s);
+  else if (few) visit_fill_launch<double, float, SHAPE_DEEP, float>(d, s);
+  else visit_fill_launch<double, float, SHAPE_WIDE, float>(d, s);
+}
 
 // Two columns per lane: whole 64-column row groups, 2-element-aligned rows
 // and pointers, uniform geometry (no explicit patch arrays).  A shard slab's
@@ -77,7 +92,7 @@ static bool visit_cpl2_ok(const VisitDesc<T>& d) {
   // fp64 Pi + Kaczmarz (the SR up visit) measured slower with two columns per
   // lane (U_16 of config 2: 270 vs 226 us; 16-byte lanes need ~220 registers
   // there); every other visit kind, and every fp32 visit, is faster
-  if (sizeof(T) == 8 && d.src == SRC_FMG && d.cr) return false;
+  if ((sizeof(T) == 8 || d.f64_arith) && d.src == SRC_FMG && d.cr) return false;
   if (visit_cpl_env() == 0 && visit_few_chains(d)) return false;
   return visit_cpl2_enabled() && d.B % 64 == 0 && d.ld % 2 == 0 && !d.olo && al(d.u_src) && al(d.uH) && al(d.uc) && al(d.f) &&
          al(d.u_out) && al(d.uH_out) && al(d.fH_out) && al(d.E) && al(d.E_out) && al(d.fun_w) &&
@@ -112,9 +127,16 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
-  if (visit_cpl2_ok(d)) visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
-  else if (visit_few_chains(d)) visit_fill_launch<T, T, SHAPE_DEEP>(d, s);
-  else visit_fill_launch<T, T, SHAPE_WIDE>(d, s);
+  if (d.f64_arith) {
+    require(!d.fun_part, "visit: no functional output with fp64 arithmetic on fp32 fields");
+    visit_launch_mixed(d, visit_cpl2_ok(d), visit_few_chains(d), s);
+  } else if (visit_cpl2_ok(d)) {
+    visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
+  } else if (visit_few_chains(d)) {
+    visit_fill_launch<T, T, SHAPE_DEEP>(d, s);
+  } else {
+    visit_fill_launch<T, T, SHAPE_WIDE>(d, s);
+  }
   check_launch("visit_kernel");
 }
 

@@ -13,7 +13,9 @@
 
 namespace fmgsr {
 
-template <typename T>
+// T: the lane's arithmetic type; M: the fields' storage type (T, or fp32
+// under fp64 arithmetic).  Edge records and functional partials stay in T.
+template <typename T, typename M = T>
 struct VisitArgs {
   i64 n, ld, W, b, P, nc, p_begin, qlo, qhi;
   T* E_out;
@@ -23,11 +25,12 @@ struct VisitArgs {
   KzCoef<T> kz;
   T inv_H2;
   bool write_u;
-  const T *u_src, *uH, *uc, *f;
-  T *u_out, *uH_out, *fH_out, *E;
+  const M *u_src, *uH, *uc, *f;
+  M *u_out, *uH_out, *fH_out;
+  T* E;
   int* cnt;
   const i64 *olo, *ohi, *elo, *ehi;
-  const T* fun_w;  // FUNC: weights (nullptr: unit)
+  const M* fun_w;  // FUNC: weights (nullptr: unit)
   T* fun_part;     // FUNC: per-(patch, column) partial sums [P][nrg * 32]
 };
 
@@ -43,17 +46,19 @@ struct VisitShape {
   static constexpr int D = SHAPE == SHAPE_WIDE ? 8 : 16;
 };
 
-template <typename T, int SRC, bool CR, int NT, int D>
-__host__ __device__ constexpr size_t visit_ring_bytes() {
-  return (size_t)D * SrcRows<SRC, CR>::R * NT * sizeof(T);
+template <typename M, int SRC, bool CR, int NT, int D>
+__host__ __device__ constexpr size_t visit_ring_bytes() {  // the ring holds stored (M) rows
+  return (size_t)D * SrcRows<SRC, CR>::R * NT * sizeof(M);
 }
-template <typename T, int SRC, bool CR, int NT, int D>
+template <typename M, int SRC, bool CR, int NT, int D>
 __host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one mbarrier per (warp, slot)
-  return visit_ring_bytes<T, SRC, CR, NT, D>() + (size_t)(NT / 32) * D * 8;
+  return visit_ring_bytes<M, SRC, CR, NT, D>() + (size_t)(NT / 32) * D * 8;
 }
 
-template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC, int NT, int D>
-__global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_kernel(const VisitArgs<T> a) {
+template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC, int NT, int D,
+          typename M = T>
+__global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT)
+    visit_kernel(const VisitArgs<T, M> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
   // 32-bit index math (a launch has < 2^32 threads): no 64-bit division at entry
@@ -84,9 +89,9 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
     we = oe + a.b < a.n ? oe + a.b : a.n;
   }
 
-  Chain<T, SRC, CR, EPI, OMEGA1, NT, D, BULK, FUNC> ch;
+  Chain<T, SRC, CR, EPI, OMEGA1, NT, D, BULK, FUNC, M> ch;
   ch.lane = lane;
-  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<T, SRC, CR, NT, D>()) +
+  ch.bars = reinterpret_cast<unsigned long long*>(visit_smem + visit_ring_bytes<M, SRC, CR, NT, D>()) +
             (threadIdx.x >> 5) * D;
   if (BULK) {
     if (lane == 0)
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
   ch.os = os;
   ch.oe = oe;
   ch.store = store;
-  ch.ring = reinterpret_cast<T*>(visit_smem) + threadIdx.x;
+  ch.ring = reinterpret_cast<M*>(visit_smem) + threadIdx.x;
   ch.out = (a.u_out && (!EPI || a.write_u)) ? a.u_out + rr : nullptr;
   ch.fw = (FUNC && a.fun_w) ? a.fun_w + rr : nullptr;
   ch.facc = T(0);
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
     if (FUNC) a.fun_part[p * ((i64)a.nrg * 32) + r] = ch.facc;
     return;
   }
-  Epilogue<T> ep;
+  Epilogue<T, M> ep;
   ep.inv_h2 = a.gc.inv_h2;
   ep.inv_H2 = a.inv_H2;
   ep.left_dom = (os == 0);
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT) visit_ke
 #pragma unroll
     for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
   }
-  edge_arrive2(a.E, a.cnt, ldE, a.nrg, lane, rg, r, store, ep.fH_out, a.ld, ep.inv_h2, ep.inv_H2,
+  edge_arrive2<T, false, M>(a.E, a.cnt, ldE, a.nrg, lane, rg, r, store, ep.fH_out, a.ld, ep.inv_h2, ep.inv_H2,
                !ep.left_dom && !remL, p, ep.left, os, !ep.right_dom && !remR, p + 1, right, oe);
 }
 
@@ -167,12 +172,12 @@ static bool visit_bulk_enabled() {
 }
 
 
-template <typename T, int SHAPE, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK,
+template <typename T, typename M, int SHAPE, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK,
           bool FUNC = false>
-static void launch_visit_k(const VisitArgs<T>& a, cudaStream_t s) {
+static void launch_visit_k(const VisitArgs<T, M>& a, cudaStream_t s) {
   constexpr int NT = VisitShape<SHAPE>::NT, D = VisitShape<SHAPE>::D;
-  constexpr size_t smem = visit_smem_bytes<T, SRC, CR, NT, D>();
-  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC, NT, D>;
+  constexpr size_t smem = visit_smem_bytes<M, SRC, CR, NT, D>();
+  auto k = visit_kernel<T, SRC, CR, EPI, OMEGA1, BULK, FUNC, NT, D, M>;
   if (smem > 48 * 1024)
     require(smem <= (size_t)smem_optin((const void*)k), "visit: shared memory budget exceeded");
   const i64 warps = a.P * a.nrg;
@@ -181,16 +186,16 @@ static void launch_visit_k(const VisitArgs<T>& a, cudaStream_t s) {
 }
 
 // Bulk (TMA) staging needs whole 32-column row segments at 16-byte alignment.
-template <typename T>
-static bool bulk_ok(const VisitArgs<T>& a) {
+template <typename T, typename M>
+static bool bulk_ok(const VisitArgs<T, M>& a) {
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  return a.B % 32 == 0 && (a.ld * sizeof(T)) % 16 == 0 && al(a.f) &&
+  return a.B % 32 == 0 && (a.ld * sizeof(M)) % 16 == 0 && al(a.f) &&
          (!a.u_src || al(a.u_src)) && (!a.uH || al(a.uH)) && (!a.uc || al(a.uc)) &&
          visit_bulk_enabled();
 }
 
-template <typename T, int SHAPE, int SRC, bool CR, bool EPI>
-static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
+template <typename T, typename M, int SHAPE, int SRC, bool CR, bool EPI>
+static void launch_visit_t(const VisitArgs<T, M>& a, cudaStream_t s) {
   const bool om1 = a.gc.omega == T(1);
   // bulk (TMA) staging pays off where per-lane LDGSTS saturates the MIO
   // queue: sources with >= 5 staged rows per pair (the FAS-correction visits);
@@ -201,7 +206,7 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   // default for B % 64 == 0) per-lane 16-byte cp.async measured faster on
   // every config (config 2 / 4 / 5: +0.3 / +1.5 / +1.6 % per cycle), and fp32
   // lanes likewise (config 5 fp32: level-19 up 452 -> 379 us)
-  constexpr bool bulk_lanes = std::is_same<T, double>::value;
+  constexpr bool bulk_lanes = std::is_same<T, double>::value && std::is_same<M, double>::value;
   // and only with more warps than SM sub-partitions: a warp issuing alone
   // waits on lane 0's serial bulk issue every pair (an 8-way shard of config 4,
   // U_23 with scalar lanes: 19 % of the stall samples on the mbarrier wait)
@@ -211,33 +216,36 @@ static void launch_visit_t(const VisitArgs<T>& a, cudaStream_t s) {
   if constexpr (!EPI && ((SRC == SRC_FMG && CR) || (SRC == SRC_CORR && !CR))) {
     if (a.fun_part) {
       if (om1) {
-        if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, true, true, true>(a, s);
-        else launch_visit_k<T, SHAPE, SRC, CR, EPI, true, false, true>(a, s);
+        if (bulk) launch_visit_k<T, M, SHAPE, SRC, CR, EPI, true, true, true>(a, s);
+        else launch_visit_k<T, M, SHAPE, SRC, CR, EPI, true, false, true>(a, s);
       } else {
-        if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, false, true, true>(a, s);
-        else launch_visit_k<T, SHAPE, SRC, CR, EPI, false, false, true>(a, s);
+        if (bulk) launch_visit_k<T, M, SHAPE, SRC, CR, EPI, false, true, true>(a, s);
+        else launch_visit_k<T, M, SHAPE, SRC, CR, EPI, false, false, true>(a, s);
       }
       return;
     }
   }
   if (om1) {
-    if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, true, true>(a, s);
-    else launch_visit_k<T, SHAPE, SRC, CR, EPI, true, false>(a, s);
+    if (bulk) launch_visit_k<T, M, SHAPE, SRC, CR, EPI, true, true>(a, s);
+    else launch_visit_k<T, M, SHAPE, SRC, CR, EPI, true, false>(a, s);
   } else {
-    if (bulk) launch_visit_k<T, SHAPE, SRC, CR, EPI, false, true>(a, s);
-    else launch_visit_k<T, SHAPE, SRC, CR, EPI, false, false>(a, s);
+    if (bulk) launch_visit_k<T, M, SHAPE, SRC, CR, EPI, false, true>(a, s);
+    else launch_visit_k<T, M, SHAPE, SRC, CR, EPI, false, false>(a, s);
   }
 }
 
 
 // Fill the kernel arguments for lane type TV (T, or V2<T>: two columns per
 // lane) from a validated descriptor and launch.
-template <typename TV, typename T, int SHAPE>
+// TM: the lane's storage type (TV, or the fp32 twin of an fp64 lane type
+// under fp64 arithmetic); edge records (d.E, d.E_out) then hold TV values.
+template <typename TV, typename T, int SHAPE, typename TM = TV>
 void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   constexpr int C = LaneCols<TV>::value;
-  auto cv = [](const T* p) { return reinterpret_cast<const TV*>(p); };
-  auto mv = [](T* p) { return reinterpret_cast<TV*>(p); };
-  VisitArgs<TV> a;
+  auto cv = [](const T* p) { return reinterpret_cast<const TM*>(p); };
+  auto mv = [](T* p) { return reinterpret_cast<TM*>(p); };
+  auto rv = [](T* p) { return reinterpret_cast<TV*>(p); };
+  VisitArgs<TV, TM> a;
   a.n = d.n;
   a.ld = d.ld / C;
   a.B = d.B / C;
@@ -254,7 +262,7 @@ void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   a.u_out = mv(d.u_out);
   a.uH_out = mv(d.uH_out);
   a.fH_out = mv(d.fH_out);
-  a.E = mv(d.E);
+  a.E = rv(d.E);
   a.cnt = d.cnt;
   a.olo = d.olo;
   a.ohi = d.ohi;
@@ -263,11 +271,11 @@ void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   a.p_begin = 0;
   a.qlo = d.qlo >= 0 ? d.qlo : 0;
   a.qhi = d.qhi >= 0 ? d.qhi : a.nc - 1;
-  a.E_out = mv(d.E_out);
+  a.E_out = rv(d.E_out);
   a.left_remote = d.left_remote;
   a.right_remote = d.right_remote;
   a.fun_w = cv(d.fun_w);
-  a.fun_part = mv(d.fun_part);
+  a.fun_part = rv(d.fun_part);
   if (d.olo) {
     a.P = d.P;
     a.W = 0;
@@ -284,11 +292,11 @@ void visit_fill_launch(const VisitDesc<T>& d, cudaStream_t s) {
   if (a.P == 0) return;
 #define FMGSR_DISPATCH(SRCV)                                                    \
   if (d.cr) {                                                                  \
-    if (d.epi) launch_visit_t<TV, SHAPE, SRCV, true, true>(a, s);                     \
-    else launch_visit_t<TV, SHAPE, SRCV, true, false>(a, s);                          \
+    if (d.epi) launch_visit_t<TV, TM, SHAPE, SRCV, true, true>(a, s);                     \
+    else launch_visit_t<TV, TM, SHAPE, SRCV, true, false>(a, s);                          \
   } else {                                                                     \
-    if (d.epi) launch_visit_t<TV, SHAPE, SRCV, false, true>(a, s);                    \
-    else launch_visit_t<TV, SHAPE, SRCV, false, false>(a, s);                         \
+    if (d.epi) launch_visit_t<TV, TM, SHAPE, SRCV, false, true>(a, s);                    \
+    else launch_visit_t<TV, TM, SHAPE, SRCV, false, false>(a, s);                         \
   }
   if (d.src == SRC_LOAD) {
     FMGSR_DISPATCH(SRC_LOAD)

@@ -146,7 +146,7 @@ def _operator_path(cfg, forcing, collect_diagnostics, debug_sr):
 
 def fmg_solve(cfg: SolverConfig, forcing, exact=None, collect_diagnostics: bool = False,
               debug_sr: bool = False, keep_state: bool = False, fused: bool = True,
-              coarse: int = -1):
+              coarse: int = -1, arith=None):
     """One full-multigrid pass (cycles.py:137-222) for one or B right-hand sides.
 
     ``forcing`` is (2**m,) or (2**m, B).  Returns (solution, Diagnostics).
@@ -154,7 +154,9 @@ def fmg_solve(cfg: SolverConfig, forcing, exact=None, collect_diagnostics: bool 
     maximum over right-hand sides for a batch).  ``fused`` / ``coarse`` select
     the native plan's kernels (fused level visits; on-chip coarse hierarchy
     with automatic cutoff (-1), off (0) or cutoff level ``coarse - 1``); all
-    choices give bit-identical results.
+    choices give bit-identical results.  ``arith=torch.float64`` with a
+    float32 forcing keeps every level field in fp32 and computes in fp64
+    (native plan only).
     """
     m = cfg.hierarchy.m
     if F.length(forcing) != 2 ** m:
@@ -163,11 +165,14 @@ def fmg_solve(cfg: SolverConfig, forcing, exact=None, collect_diagnostics: bool 
     Fd = F.to_field(forcing, dt)
     f = Fd.t
     if collect_diagnostics or debug_sr or keep_state:
+        if arith is not None and arith != dt:
+            raise ValueError("arith differs from the field dtype: native plan only "
+                             "(no diagnostics / debug_sr / keep_state)")
         sol, diag, state = _operator_path(cfg, f, collect_diagnostics, debug_sr)
         if keep_state:
             diag.state = state
     else:
-        plan = get_plan(key_from_config(cfg, Fd.B, dt, fused=fused, coarse=coarse))
+        plan = get_plan(key_from_config(cfg, Fd.B, dt, fused=fused, coarse=coarse, arith=arith))
         sol = plan.solve(f)
         diag = Diagnostics()
     if exact is not None:

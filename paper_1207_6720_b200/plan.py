@@ -37,10 +37,29 @@ class PlanKey:
     use_graph: bool = True
     coarse: int = -1  # on-chip coarse hierarchy: -1 auto, 0 off, k > 0 cutoff level k - 1
     nonlinear: bool = False  # -u'' + u^3 = f
+    # arithmetic type (None: the field dtype); float32 fields with float64
+    # arithmetic store every level in fp32 and compute in fp64 (dtype code 2)
+    arith: torch.dtype | None = None
+
+
+def dtype_code(key: "PlanKey") -> int:
+    """The C ABI's dtype: 0 = f64, 1 = f32, 2 = f32 fields with f64 arithmetic."""
+    if key.dtype == torch.float64:
+        if key.arith not in (None, torch.float64):
+            raise ValueError("float64 fields need float64 arithmetic")
+        return 0
+    if key.dtype != torch.float32:
+        raise ValueError(f"unsupported field dtype {key.dtype}")
+    if key.arith in (None, torch.float32):
+        return 1
+    if key.arith == torch.float64:
+        return 2
+    raise ValueError(f"unsupported arithmetic dtype {key.arith}")
 
 
 def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
-                    use_graph: bool = True, coarse: int = -1) -> PlanKey:
+                    use_graph: bool = True, coarse: int = -1,
+                    arith: torch.dtype | None = None) -> PlanKey:
     """PlanKey of a ``cycles.SolverConfig`` for a batch of B right-hand sides."""
     from .mesh import HaloMode
 
@@ -54,7 +73,8 @@ def key_from_config(cfg, B: int, dtype: torch.dtype, fused: bool = True,
         mode, P = GEOM_HALO, 1
         b = sm.buffer if sm.buffer is not None else sm.halo_mode.halo
     return PlanKey(cfg.hierarchy.m0, cfg.hierarchy.m, cfg.n_sr, sm.ns, mode, int(P), int(b),
-                   int(B), dtype, float(sm.omega), fused, use_graph, coarse, bool(sm.nonlinear))
+                   int(B), dtype, float(sm.omega), fused, use_graph, coarse, bool(sm.nonlinear),
+                   None if arith == dtype else arith)
 
 
 class FmgPlan:
@@ -64,7 +84,7 @@ class FmgPlan:
         d = N.PlanDesc()
         d.m0, d.m, d.n_sr, d.ns = key.m0, key.m, key.n_sr, key.ns
         d.geom_mode = key.geom_mode
-        d.dtype = 0 if key.dtype == torch.float64 else 1
+        d.dtype = dtype_code(key)
         d.P, d.b, d.B, d.ld = key.P, key.b, key.B, key.B
         d.omega = key.omega
         d.fused = int(key.fused)

@@ -21,14 +21,14 @@ import ctypes as C
 import torch
 
 from . import _native as N
-from .plan import PlanKey, key_from_config
+from .plan import PlanKey, dtype_code, key_from_config
 
 
 def _desc(key: PlanKey) -> N.PlanDesc:
     d = N.PlanDesc()
     d.m0, d.m, d.n_sr, d.ns = key.m0, key.m, key.n_sr, key.ns
     d.geom_mode = key.geom_mode
-    d.dtype = 0 if key.dtype == torch.float64 else 1
+    d.dtype = dtype_code(key)
     d.P, d.b, d.B, d.ld = key.P, key.b, key.B, key.B
     d.omega = key.omega
     d.fused = int(key.fused)

@@ -35,7 +35,7 @@ cfg = fm.SolverConfig(hierarchy=fm.build_hierarchy(w["m0"], w["m"]), n_sr=w["n_s
                       smoother=fm.SmootherConfig(ns=w["ns"], n_patches=w["P"], buffer=w["b"],
                                                  nonlinear=nl))
 if not a.shards:
-    plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused,
+    plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused, arith=bench._arith(w),
                                           use_graph=a.graph))
 if nl:
     f, _ = fm.nonlinear_batch(2 ** w["m"], fm.nonlinear_scales(w["B"]), dt)

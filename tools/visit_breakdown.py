@@ -50,7 +50,8 @@ if a.shards:
     rows = 2 ** w["m"] // a.shards
     f = f[a.rank * rows:(a.rank + 1) * rows].contiguous()
 else:
-    plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused))
+    plan = fm.get_plan(fm.key_from_config(cfg, w["B"], dt, fused=not a.unfused,
+                                          arith=bench._arith(w)))
 sol = torch.empty_like(f)
 for _ in range(2):
     plan.solve(f, sol)
