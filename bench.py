@@ -421,8 +421,21 @@ def _init_dist(world, local, backend="nccl"):
             dist.init_process_group(backend)
 
 
-def run_gpu(args, w):
-    """N = 1 (and the ``--shard rhs`` control at N > 1): every rank solves its own batch."""
+def all_ok(ok: bool, world: int, device: str = "cuda") -> bool:
+    """True iff ``ok`` holds on every rank (MIN over ranks)."""
+    if world <= 1:
+        return bool(ok)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def run_gpu(args, w, note=None):
+    """N = 1 (and the ``--shard rhs`` control at N > 1): every rank solves its own batch.
+    ``note``: extra keys for the JSON line (the sharded path's failure, if it fell back)."""
     import torch
     import torch.distributed as dist
 
@@ -553,6 +566,8 @@ def run_gpu(args, w):
                        "solution is never stored)"}
         if extra:
             line["config2"] = extra
+        if note:
+            line.update(note)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -586,23 +601,45 @@ def run_gpu_sharded(args, w):
     check_world(args.gpus, world)
     if world == 1:
         return run_gpu(args, w)
+    # FMGSR_BENCH_BACKEND=gloo: functional check of the plumbing with several
+    # ranks on one GPU (the sharded plan's own NCCL communicator then refuses
+    # the shared device, which exercises the fall-back; never a measurement)
+    backend = os.environ.get("FMGSR_BENCH_BACKEND", "nccl")
+    cdev = "cuda" if backend == "nccl" else "cpu"
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
-    _init_dist(world, local)
+    _init_dist(world, local, backend)
     dtype = torch.float64 if w["dtype"] == "f64" else torch.float32
     m, B = w["m"], w["B"]
     n = 2 ** m
     cfg = _solver_cfg(fm, w)
-    uid = broadcast_uid(nccl_unique_id() if rank == 0 else None, rank)
-    plan = ShardedPlan(cfg, B, world, rank, uid, dtype)
     c0, c1 = slab(n, world, rank)
-    f = _forcing(fm, w, dtype, 0)  # the one problem (same seed on every rank)
-    fs = f[c0:c1].contiguous()
-    del f
-    sol = torch.empty_like(fs)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        plan.solve(fs, sol)
-    torch.cuda.synchronize()
+    # Build the sharded plan and run the warm-ups; if that fails on any rank
+    # (no NCCL library, a geometry the split cannot take, a CUDA or NCCL
+    # error), every rank falls back to the independent-RHS split and the line
+    # says why.  (A failure here is raised by the NCCL calls, not hung: every
+    # send has its matching receive, tests/test_shard_schedule.py.)
+    plan, fs, sol, err = None, None, None, None
+    try:
+        uid = broadcast_uid(nccl_unique_id() if rank == 0 else None, rank, device=cdev)
+        plan = ShardedPlan(cfg, B, world, rank, uid, dtype)
+        f = _forcing(fm, w, dtype, 0)  # the one problem (same seed on every rank)
+        fs = f[c0:c1].contiguous()
+        del f
+        sol = torch.empty_like(fs)
+        for _ in range(args.warmup):
+            plan.solve(fs, sol)
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001 -- reported in the line, never hidden
+        err = f"{type(e).__name__}: {e}"
+    if not all_ok(err is None, world, device=cdev):
+        del plan, fs, sol
+        torch.cuda.empty_cache()
+        return run_gpu(args, w, note={
+            "sharded_error": err or "failed on another rank",
+            "sharded_fallback": "patch-slab split unavailable; independent RHS batches per GPU"})
     clk = ClockSampler(local)
     ms_step = _timed(lambda: plan.solve(fs, sol), args.steps, world, stream, dist.barrier)
     clocks = clk.stop()
@@ -622,17 +659,27 @@ def run_gpu_sharded(args, w):
     torch.cuda.synchronize()
     e2e_ms = _timed(e2e_step, args.steps, world, stream, dist.barrier)
     info = plan.info()
-    del hf, hs, dfi, sol, fs, plan
+    plan.solve(fs, sol)  # the timed solves' result, kept for the parity check
+    sol_keep = sol
+    del hf, hs, dfi, fs, plan
     torch.cuda.empty_cache()
     esz = 8 if dtype == torch.float64 else 4
     peak, peak_src = measured_peak()
     alg = info["alg_bytes_per_solve"]  # whole problem (29 words / unknown)
 
     # ---- control: every rank its own batch (weak scaling, no data-path collective) --
-    control = None
+    # plus the parity check of the split: the unsharded plan on the same forcing,
+    # this rank's rows compared bit for bit with its slab of the sharded solve
+    control, eq_local = None, None
     if not args.no_extra:
         try:
             p1 = fm.get_plan(fm.key_from_config(cfg, B, dtype, arith=_arith(w)))
+            f1 = _forcing(fm, w, dtype, 0)
+            s1 = torch.empty_like(f1)
+            p1.solve(f1, s1)
+            torch.cuda.synchronize()
+            eq_local = bool(torch.equal(s1[c0:c1], sol_keep))
+            del f1, s1
             f1 = _forcing(fm, w, dtype, rank_seed(rank))
             s1 = torch.empty_like(f1)
             for _ in range(args.warmup):
@@ -645,6 +692,8 @@ def run_gpu_sharded(args, w):
             del p1, f1, s1
         except Exception as e:  # the control never hides the headline
             control = {"error": str(e)}
+    exact = None if args.no_extra else all_ok(bool(eq_local), world, device=cdev)
+    del sol_keep
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -665,6 +714,7 @@ def run_gpu_sharded(args, w):
             "gpu_launches": info["launches_per_solve"] * args.steps,
             "clocks": clocks, "cpu_baseline": None,
             "control_rhs_batch": control,
+            "sharded_bit_exact_vs_unsharded": exact,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

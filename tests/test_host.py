@@ -188,14 +188,17 @@ def _shard_rank_main(rank, world, port, q):
     uid = bytes(range(128)) if rank == 0 else None  # stands in for ncclGetUniqueId
     got = bench.broadcast_uid(uid, rank, device="cpu")
     n = 2 ** 24
-    q.put((rank, got, slab(n, world, rank)))
+    # the fall-back vote of run_gpu_sharded: one failing rank moves every rank
+    votes = (bench.all_ok(True, world, device="cpu"), bench.all_ok(rank != world - 1, world, device="cpu"))
+    q.put((rank, got, slab(n, world, rank), votes))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_host_side_gloo(world):
-    """run_gpu_sharded's host side: rank 0's NCCL id reaches every rank, and the
-    slabs tile the finest level exactly once."""
+    """run_gpu_sharded's host side: rank 0's NCCL id reaches every rank, the
+    slabs tile the finest level exactly once, and a failure on one rank makes
+    every rank take the fall-back (all_ok is a MIN over ranks)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29700 + (os.getpid() % 500) + world
@@ -207,6 +210,7 @@ def test_sharded_host_side_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(r[1] == bytes(range(128)) for r in res)
+    assert all(r[3] == (True, False) for r in res)
     spans = [r[2] for r in res]
     assert spans[0][0] == 0 and spans[-1][1] == 2 ** 24
     assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
