@@ -133,6 +133,15 @@ int fmgsr_direct_solve_f32(const float* f, float* u, int64_t n, int64_t B, int64
  * (also backs problem.direct_fine_solve, problem.py:61-77) */
 int fmgsr_direct_solve_ws_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, double* workspace, void* stream);
 int fmgsr_direct_solve_ws_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* workspace, void* stream);
+/* direct_fine_solve, problem.py:61-77: the reference's INDEPENDENT check
+ * solve (scipy solve_banded((1, 1)) -> LAPACK dgbsv: banded LU with partial
+ * pivoting, then dgbtrs), restated in that operation order.  DEVICE workspace
+ * of 2n elements (the factor); *pivots (device int, zeroed by the caller)
+ * receives the number of row swaps the pivot search would have made -- none
+ * for this operator; a non-zero count means the result is not the
+ * reference's and the caller must reject it. */
+int fmgsr_banded_lu_solve_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, double* workspace, int* pivots, void* stream);
+int fmgsr_banded_lu_solve_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* workspace, int* pivots, void* stream);
 
 /* ---- Fused level visits and the f cascade -------------------
  * The plan's level-visit kernels, one call per visit, for a caller that drives

@@ -72,6 +72,8 @@ def lib():
         _lib.orc_tau_correction.argtypes = [_dp, _dp, _i64, _dp]
         _lib.orc_coarse_rhs.argtypes = [_dp, _dp, _dp, _i64, _dp]
         _lib.orc_direct_solve.argtypes = [_dp, _dp, _i64, _dp]
+        _lib.orc_banded_lu_solve.argtypes = [_dp, _dp, _i64, _dp]
+        _lib.orc_banded_lu_solve.restype = C.c_int
         _lib.orc_fmg_solve.argtypes = [C.POINTER(OrcCfg), _dp, _dp]
         _lib.orc_fmg_solve_batch.argtypes = [C.POINTER(OrcCfg), _dp, _dp, _i64, C.c_int]
         _lib.orc_level_geometry.argtypes = [_i64, C.c_int, _i64, _i64, _ip, _ip]
@@ -175,6 +177,16 @@ def direct_solve(f):
     out = np.empty_like(f)
     work = np.empty(2 * len(f) + 2)
     lib().orc_direct_solve(_d(f), _d(out), len(f), _d(work))
+    return out
+
+
+def banded_lu_solve(f):
+    """problem.py:61-77 direct_fine_solve (LAPACK dgbsv order)."""
+    f = _f64(f)
+    out = np.empty_like(f)
+    work = np.empty(2 * len(f) + 2)
+    if lib().orc_banded_lu_solve(_d(f), _d(out), len(f), _d(work)):
+        raise RuntimeError("banded LU: the pivot search would swap rows")
     return out
 
 

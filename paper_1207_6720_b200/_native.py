@@ -90,6 +90,7 @@ _SIGS = {
     "fmgsr_f_cascade": (C.c_int, [_vp, _i64, _i64, _i64, _i32, C.POINTER(_vp), _vp]),
     "fmgsr_direct_solve": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "fmgsr_direct_solve_ws": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "fmgsr_banded_lu_solve": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_fourier_rhs": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_nonlinear_rhs": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "fmgsr_smooth_scratch_rows": (_i64, [_i64, _i64, _i64]),
@@ -120,8 +121,8 @@ _SIGS = {
 _TYPED = {"fmgsr_gs_sweep", "fmgsr_kaczmarz_sweep", "fmgsr_smooth_patches", "fmgsr_smooth_uniform",
           "fmgsr_apply_operator", "fmgsr_restrict", "fmgsr_prolong_correction",
           "fmgsr_prolong_fmg", "fmgsr_tau_correction", "fmgsr_coarse_rhs", "fmgsr_fas_correct",
-          "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_fourier_rhs",
-          "fmgsr_nonlinear_rhs", "fmgsr_smooth_uniform_nl", "fmgsr_coarse_rhs_nl",
+          "fmgsr_direct_solve", "fmgsr_direct_solve_ws", "fmgsr_banded_lu_solve",
+          "fmgsr_fourier_rhs", "fmgsr_nonlinear_rhs", "fmgsr_smooth_uniform_nl", "fmgsr_coarse_rhs_nl",
           "fmgsr_direct_solve_nl", "fmgsr_div_check", "fmgsr_visit_top", "fmgsr_visit_down",
           "fmgsr_visit_up", "fmgsr_f_cascade"}
 

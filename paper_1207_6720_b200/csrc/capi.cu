@@ -1954,6 +1954,12 @@ int fmgsr_direct_solve_ws_f64(const double* f, double* u, int64_t n, int64_t B, 
 int fmgsr_direct_solve_ws_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* ws, void* s) {
   return guarded([&] { check_field(n, B, ld, "direct_solve"); require(ws != nullptr, "direct_solve_ws: null workspace"); launch_direct_solve<float>(f, u, n, ld, (int)B, S(s), ws); });
 }
+int fmgsr_banded_lu_solve_f64(const double* f, double* u, int64_t n, int64_t B, int64_t ld, double* ws, int* piv, void* s) {
+  return guarded([&] { check_field(n, B, ld, "banded_lu_solve"); launch_banded_lu_solve<double>(f, u, n, ld, (int)B, ws, piv, S(s)); });
+}
+int fmgsr_banded_lu_solve_f32(const float* f, float* u, int64_t n, int64_t B, int64_t ld, float* ws, int* piv, void* s) {
+  return guarded([&] { check_field(n, B, ld, "banded_lu_solve"); launch_banded_lu_solve<float>(f, u, n, ld, (int)B, ws, piv, S(s)); });
+}
 int fmgsr_nonlinear_rhs_f64(const double* scale, int64_t n, int64_t B, int64_t ld, double* f, double* uex, void* s) {
   return guarded([&] { check_field(n, B, ld, "nonlinear_rhs"); launch_nonlinear_rhs<double>(scale, n, ld, (int)B, f, uex, S(s)); });
 }

@@ -265,6 +265,7 @@ template <typename T> void launch_restrict_tau(const T* u, const T* f, T* uH_out
 template <typename T> void launch_direct_solve_nl(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s, T* workspace = nullptr);
+template <typename T> void launch_banded_lu_solve(const T* f, T* u, i64 n, i64 ld, int B, T* workspace, int* bad, cudaStream_t s);
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);
 template <typename T> void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop, double proj_diag, cudaStream_t s);
 template <typename T> void launch_fourier_rhs(const double* coef, int K, i64 n, i64 ld, int B, T* f, T* uex, cudaStream_t s);

@@ -315,6 +315,75 @@ __global__ void k_direct_solve(const T* __restrict__ f, T* __restrict__ u, i64 n
   }
 }
 
+// problem.py:61-77 direct_fine_solve -> scipy solve_banded((1, 1), ab, f) ->
+// LAPACK dgbsv: dgbtf2 (LU with partial pivoting; multipliers are the
+// sub-diagonal scaled by RN(1/pivot) as DSCAL does; the trailing update is the
+// DGER rank-1 step a + l * (-(super))), then dgbtrs (the DGER forward sweep
+// b_{j+1} + l_j * (-b_j), skipped when b_j == 0, and DTBSV's upper back
+// substitution over the KL + KU = 2 superdiagonals, the second being the
+// zero fill-in).  An algorithm independent of the L D L^T coarse solve above,
+// as the reference intends ("general LU here, Cholesky there").  This
+// operator is strictly diagonally dominant after the first column, so the
+// pivot search never swaps rows; the factor kernel checks that and flags it.
+template <typename T>
+__global__ void k_gb_factor(T* fac, i64 n, int* bad) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const T ih = inv_h2_of<T>(n);
+  T* u = fac;      // pivots u_jj
+  T* l = fac + n;  // multipliers l_j (row j+1 of column j)
+  T dj = xmul(T(3), ih);
+  int swaps = 0;
+  for (i64 j = 0; j < n; j++) {
+    u[j] = dj;
+    if (j == n - 1) break;
+    const T sub = -ih;
+    if (fabs(sub) > fabs(dj)) swaps++;  // IDAMAX would pick the sub-diagonal
+    const T lj = xmul(xrcp(dj), sub);   // DSCAL(1, ONE / AB(KV+1, J), ...)
+    l[j] = lj;
+    const T temp = -sub;                // DGER: TEMP = -ONE * A(J, J+1)
+    const T a = (j + 1 == n - 1) ? xmul(T(3), ih) : xmul(T(2), ih);
+    dj = xadd(a, xmul(lj, temp));
+  }
+  if (swaps) atomicAdd(bad, swaps);
+}
+
+template <typename T>
+__global__ void k_gb_solve(const T* __restrict__ f, T* __restrict__ x, i64 n, i64 ld, int B,
+                           const T* __restrict__ fac) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= B) return;
+  const T ih = inv_h2_of<T>(n);
+  const T* u = fac;
+  const T* l = fac + n;
+  const T* fr = f + r;
+  T* xr = x + r;
+  // dgbtrs forward: DGER(1, NRHS, -ONE, l_j, 1, B(J, :), LDB, B(J+1, :), LDB)
+  T prev = fr[0];
+  xr[0] = prev;
+  for (i64 j = 0; j + 1 < n; j++) {
+    T b = fr[(j + 1) * ld];
+    if (prev != T(0)) b = xadd(b, xmul(l[j], -prev));
+    xr[(j + 1) * ld] = b;
+    prev = b;
+  }
+  // DTBSV('U', 'N', 'N', n, 2, AB, LDAB, x): column-oriented back substitution;
+  // c0 = x_j (final input), c1 = x_{j-1} (after step j+1's update)
+  const T sup = -ih;
+  T c0 = prev;
+  T c1 = n >= 2 ? xr[(n - 2) * ld] : T(0);
+  for (i64 j = n - 1; j >= 0; j--) {
+    T c2 = j >= 2 ? xr[(j - 2) * ld] : T(0);
+    if (c0 != T(0)) {
+      c0 = xdiv(c0, u[j]);
+      c1 = xsub(c1, xmul(c0, sup));
+      c2 = xsub(c2, xmul(c0, T(0)));  // the zero fill-in row of the band
+    }
+    xr[j * ld] = c0;
+    c0 = c1;
+    c1 = c2;
+  }
+}
+
 // _kernels_numba.py:15-36, one thread per RHS, in place
 template <typename T>
 __global__ void k_gs_sweep(T* u, const T* __restrict__ f, i64 n, i64 ld, int B, GsCoef<T> gc,
@@ -549,6 +618,16 @@ void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s,
   check_launch("direct_solve");
 }
 template <typename T>
+void launch_banded_lu_solve(const T* f, T* u, i64 n, i64 ld, int B, T* workspace, int* bad,
+                            cudaStream_t s) {
+  require(n >= 2 && is_pow2(n), "banded_lu_solve: size must be a power of two >= 2");
+  require(workspace != nullptr && bad != nullptr, "banded_lu_solve: null workspace");
+  k_gb_factor<T><<<1, 1, 0, s>>>(workspace, n, bad);
+  check_launch("gb_factor");
+  k_gb_solve<T><<<(B + 127) / 128, 128, 0, s>>>(f, u, n, ld, B, workspace);
+  check_launch("gb_solve");
+}
+template <typename T>
 void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop,
                      bool forward, double omega, cudaStream_t s) {
   require(0 <= start && start < stop && stop <= n, "gs_sweep: window outside [0, n)");
@@ -626,6 +705,7 @@ void launch_div_check(const T* x, const T* J, T* q, i64 n, unsigned long long* b
   template void launch_direct_solve_nl<T>(const T*, T*, i64, i64, int, cudaStream_t);          \
   template void launch_fas_correct<T>(const T*, const T*, T*, i64, i64, int, cudaStream_t);   \
   template void launch_direct_solve<T>(const T*, T*, i64, i64, int, cudaStream_t, T*);            \
+  template void launch_banded_lu_solve<T>(const T*, T*, i64, i64, int, T*, int*, cudaStream_t);  \
   template void launch_gs_sweep<T>(T*, const T*, i64, i64, int, double, i64, i64, bool,       \
                                    double, cudaStream_t);                                      \
   template void launch_kaczmarz_sweep<T>(T*, const T*, i64, i64, int, i64, i64, double,       \

@@ -84,11 +84,23 @@ def rel_l2_error(u, u_ref) -> float:
 def direct_fine_solve(forcing):
     """Exact solve of the level operator at the forcing's level (problem.py:61-77).
 
-    The reference uses a general banded LU here as an independent check of
-    its Cholesky-type coarse solve; on the device both run the SPD
-    tridiagonal (L D L^T) solve, one thread per right-hand side."""
+    Like the reference, an algorithm independent of the coarse solve
+    (smoothers.direct_solve, L D L^T in LAPACK ?ptsv order): the general
+    banded LU of scipy's solve_banded((1, 1)) -> LAPACK dgbsv (dgbtf2 + dgbtrs)
+    in that operation order on the device (fmgsr_banded_lu_solve), one thread
+    per right-hand side, so the two can cross-check each other."""
     level_of(forcing)
-    return direct_solve(forcing)
+    dt = F.pick_dtype(forcing)
+    Fd = F.to_field(forcing, dt)
+    out = torch.empty_like(Fd.t)
+    ws = torch.empty(2 * Fd.n, dtype=dt, device=Fd.t.device)
+    piv = torch.zeros(1, dtype=torch.int32, device=Fd.t.device)
+    N.call("fmgsr_banded_lu_solve", dt, Fd.ptr(), out.data_ptr(), Fd.n, Fd.B, Fd.ld,
+           ws.data_ptr(), piv.data_ptr(), N.stream_ptr())
+    if int(piv.item()):
+        raise RuntimeError("direct_fine_solve: the pivot search would swap rows "
+                           "(not the reference's operator)")
+    return F.out(out, Fd)
 
 
 # ---- BASELINE generators --------------------------------------------------------------

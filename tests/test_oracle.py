@@ -43,6 +43,17 @@ def test_direct_solve_is_lapack_ptsv_bitwise(oracle, n):
         assert np.array_equal(oracle.direct_solve(f), solveh_banded(ab, f))
 
 
+def test_banded_lu_matches_reference_direct_fine_solve(oracle):
+    """orc_banded_lu_solve against the reference's own direct_fine_solve
+    (problem.py:61-77, scipy solve_banded -> LAPACK dgbsv), bit for bit."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "direct_fine.npz"))
+    for n in (4, 8, 16, 64, 256, 1024):
+        for f, u in zip(g[f"n{n}/f"], g[f"n{n}/u"]):
+            assert np.array_equal(oracle.banded_lu_solve(f), u)
+
+
 def test_sweeps_match_golden(oracle, golden):
     s = "sweeps/"
     u, f, uc, ih = golden[s + "u"], golden[s + "f"], golden[s + "uc"], float(golden[s + "inv_h2"])
