@@ -315,6 +315,23 @@ int fmgsr_plan_solve_timed(void* plan, const void* forcing, void* solution, void
 int fmgsr_nccl_unique_id(void* id /* 128 bytes */);
 int fmgsr_shard_plan_create(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
                             const void* nccl_id, void** plan);
+/* One shard per GPU over PEER MEMORY instead of NCCL: every rank maps its
+ * peers' plan workspaces (CUDA IPC; NVLink peer access across GPUs) and pulls
+ * the neighbours' halo rows and tau edge records, and every rank's chunk of the
+ * replication cutoff level, straight into its own arrays; ordering by
+ * per-rank device counters (release / acquire at system scope), bounded waits
+ * (FMGSR_P2P_TIMEOUT_S, default 30 s; a timeout sets the status word instead
+ * of hanging).  Also works with several processes on ONE device.  Create,
+ * export this rank's blob (fmgsr_shard_p2p_export: *len = blob bytes; buf may
+ * be NULL to query), all-gather the S blobs (rank order, any host transport),
+ * import them (fmgsr_shard_p2p_import: per_rank = the blob size), then
+ * fmgsr_plan_solve on the slabs as with the NCCL plan.  fmgsr_shard_p2p_status
+ * synchronises the device and returns *err != 0 if any wait timed out. */
+int fmgsr_shard_plan_create_p2p(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                                void** plan);
+int fmgsr_shard_p2p_export(void* plan, void* buf, int64_t cap, int64_t* len);
+int fmgsr_shard_p2p_import(void* plan, const void* all, int64_t per_rank);
+int fmgsr_shard_p2p_status(void* plan, int32_t* err);
 /* Virtual shards: all S shards of one problem on the current device, run in
  * lockstep on one stream (transfers are device copies).  forcing / solution
  * are the full DEVICE [2^m][ld] arrays; the result is bit-identical to the

@@ -115,6 +115,10 @@ _SIGS = {
     "fmgsr_shard_group_cutoff": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i64)]),
     "fmgsr_shard_group_destroy": (C.c_int, [_vp]),
     "fmgsr_shard_plan_create_local": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, C.POINTER(_vp)]),
+    "fmgsr_shard_plan_create_p2p": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, C.POINTER(_vp)]),
+    "fmgsr_shard_p2p_export": (C.c_int, [_vp, _vp, _i64, C.POINTER(_i64)]),
+    "fmgsr_shard_p2p_import": (C.c_int, [_vp, _vp, _i64]),
+    "fmgsr_shard_p2p_status": (C.c_int, [_vp, C.POINTER(_i32)]),
     "fmgsr_shard_schedule": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, _vp, _i64,
                                        C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64)]),
 }

@@ -118,6 +118,16 @@ struct PlanBase {
   virtual void solve_functional(const void* in, const void* w, void* out, cudaStream_t s) = 0;
   virtual void set_debug(int flags) = 0;
   virtual i64 check_guards() = 0;
+  // peer-memory transport of a sharded plan (fmgsr_shard_plan_create_p2p)
+  virtual size_t p2p_export(void* buf, size_t cap) {
+    (void)buf, (void)cap;
+    throw Error(ERR_ARG, "not a peer-memory shard plan");
+  }
+  virtual void p2p_import(const char* all, size_t per_rank) {
+    (void)all, (void)per_rank;
+    throw Error(ERR_ARG, "not a peer-memory shard plan");
+  }
+  virtual int p2p_status() { throw Error(ERR_ARG, "not a peer-memory shard plan"); }
 };
 
 template <typename T>
@@ -243,11 +253,14 @@ struct Plan : PlanBase {
   FMGSR_PLAN_FWD(launch_functional_reduce)
 #undef FMGSR_PLAN_FWD
 
+  std::vector<std::pair<uintptr_t, size_t>> dry_allocs;  // dry plans: fake base, bytes
+  size_t n_init_allocs = 0;  // allocations made by init() (the exported workspace)
   T* alloc(size_t bytes) {
     if (dry) {
       const uintptr_t p = dry_next;
       dry_next += (bytes + 255) / 256 * 256 + 4096;
       ws_bytes += (i64)bytes;
+      dry_allocs.push_back({p, bytes ? bytes : 16});
       return (T*)p;
     }
     void* p = nullptr;
@@ -461,6 +474,7 @@ struct Plan : PlanBase {
         off += (L.n / L.W + 1) * nrg;
       }
     }
+    n_init_allocs = dry ? dry_allocs.size() : allocs.size();
     if (!dry) check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "plan stream");
   }
 
@@ -524,6 +538,12 @@ struct Plan : PlanBase {
     if (s_out) cudaStreamDestroy(s_out), s_out = nullptr;
     if (ncomm && nccl && nccl->commDestroy) nccl->commDestroy(ncomm);
     ncomm = nullptr;
+    if (p2p) {
+      for (void* q : p2p->opened) cudaIpcCloseMemHandle(q);
+      if (p2p->flags) cudaFree(p2p->flags);
+      delete p2p;
+      p2p = nullptr;
+    }
     if (!dry)
       for (void* p : allocs) cudaFree(p);
     allocs.clear();
@@ -1227,6 +1247,211 @@ struct Plan : PlanBase {
   void* ncomm = nullptr;
   void comm_nccl(const Step& st, cudaStream_t s);  // defined after NcclApi
 
+  // ---- peer-memory transport (kernels_p2p.cu) -------------------------------------
+  // Every rank maps every peer's plan workspace (CUDA IPC) and pulls: after
+  // step si a rank publishes READY, waits for its neighbours' READY, copies
+  // their boundary rows / edge records into its own halo rows / inbox (the
+  // i-th receive from p reads p's i-th send to this rank, the pairing NCCL
+  // uses), runs the slab-edge fix-ups; a gather step then publishes FIXED,
+  // waits for every rank's FIXED, copies every rank's chunk of the cutoff
+  // level, publishes DONE and waits for every rank's DONE (nobody may touch
+  // the replicated level while a peer still reads its chunk).  Sources are
+  // resolved once, at import, by replaying each peer's step list on a dry
+  // plan of that peer (same allocation sequence, fake addresses) and mapping
+  // every address to (allocation index, offset) in the peer's real workspace.
+  struct P2pState {
+    unsigned long long* flags = nullptr;          // this rank's counter words
+    std::vector<unsigned long long*> peer_flags;  // [rank] (own: flags)
+    std::vector<void*> opened;                    // IPC mappings
+    std::vector<std::vector<const char*>> recv_src;               // [step][receive i]
+    std::vector<std::vector<std::vector<const char*>>> gath_src;  // [step][gather][rank]
+    unsigned long long timeout_ns = 30ull * 1000000000ull;
+    bool ready = false;
+  };
+  P2pState* p2p = nullptr;
+  struct P2pBlob {
+    unsigned long long magic, n_alloc, guard, rank;
+    cudaIpcMemHandle_t flags;
+    cudaIpcMemHandle_t h[1];  // n_alloc handles
+  };
+  static size_t p2p_blob_bytes(size_t n_alloc) {
+    return sizeof(P2pBlob) + (n_alloc ? n_alloc - 1 : 0) * sizeof(cudaIpcMemHandle_t);
+  }
+  void p2p_init() {
+    p2p = new P2pState;
+    check_cuda(cudaMalloc(&p2p->flags, P2P_NWORDS * sizeof(unsigned long long)), "p2p flags");
+    check_cuda(cudaMemset(p2p->flags, 0, P2P_NWORDS * sizeof(unsigned long long)), "p2p flags");
+    if (const char* e = getenv("FMGSR_P2P_TIMEOUT_S")) p2p->timeout_ns = (unsigned long long)(atof(e) * 1e9);
+  }
+  size_t p2p_export(void* buf, size_t cap) override {
+    require(p2p, "p2p_export: not a peer-memory shard plan");
+    const size_t need = p2p_blob_bytes(n_init_allocs);
+    if (!buf) return need;
+    require(cap >= need, "p2p_export: buffer too small");
+    std::vector<char> tmpb(need, 0);
+    P2pBlob* b = reinterpret_cast<P2pBlob*>(tmpb.data());
+    b->magic = 0x46474d5350325031ull;  // "FGMSP2P1"
+    b->n_alloc = n_init_allocs;
+    b->guard = guards ? GUARD : 0;
+    b->rank = (unsigned long long)srank;
+    check_cuda(cudaIpcGetMemHandle(&b->flags, p2p->flags), "cudaIpcGetMemHandle (flags)");
+    for (size_t k = 0; k < n_init_allocs; k++)
+      check_cuda(cudaIpcGetMemHandle(&b->h[k], allocs[k]), "cudaIpcGetMemHandle");
+    std::memcpy(buf, tmpb.data(), need);
+    return need;
+  }
+  void p2p_import(const char* all, size_t per_rank) override {
+    require(p2p && !p2p->ready, "p2p_import: not a fresh peer-memory shard plan");
+    require(per_rank >= p2p_blob_bytes(n_init_allocs), "p2p_import: blob too small");
+    // every rank's allocation bases (user pointers) and counter words
+    std::vector<std::vector<char*>> base(S);
+    p2p->peer_flags.assign(S, nullptr);
+    for (int q = 0; q < S; q++) {
+      const P2pBlob* b = reinterpret_cast<const P2pBlob*>(all + (size_t)q * per_rank);
+      require(b->magic == 0x46474d5350325031ull && b->rank == (unsigned long long)q,
+              "p2p_import: blob of rank " + std::to_string(q) + " is not a shard plan export");
+      require(b->n_alloc == n_init_allocs && b->guard == (guards ? GUARD : 0),
+              "p2p_import: peer plans differ (descriptor, shard count or FMGSR_GUARDS)");
+      if (q == srank) {
+        for (size_t k = 0; k < n_init_allocs; k++) base[q].push_back((char*)alloc_user[k]);
+        p2p->peer_flags[q] = p2p->flags;
+        continue;
+      }
+      void* fp = nullptr;
+      check_cuda(cudaIpcOpenMemHandle(&fp, b->flags, cudaIpcMemLazyEnablePeerAccess),
+                 "cudaIpcOpenMemHandle (peer counters)");
+      p2p->opened.push_back(fp);
+      p2p->peer_flags[q] = (unsigned long long*)fp;
+      for (size_t k = 0; k < n_init_allocs; k++) {
+        void* ptr = nullptr;
+        check_cuda(cudaIpcOpenMemHandle(&ptr, b->h[k], cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle (peer workspace)");
+        p2p->opened.push_back(ptr);
+        base[q].push_back((char*)ptr + b->guard);
+      }
+    }
+    // replay every rank's step list on a dry plan of that rank
+    const std::vector<Step> stl = steps();
+    const size_t NS = stl.size();
+    std::vector<std::vector<std::vector<Xfer>>> xs_of(S, std::vector<std::vector<Xfer>>(NS));
+    std::vector<std::vector<std::vector<Gather>>> gs_of(S, std::vector<std::vector<Gather>>(NS));
+    std::vector<std::unique_ptr<Plan<T>>> dryp(S);
+    for (int q = 0; q < S; q++) {
+      dryp[q].reset(new Plan<T>(d, S, q, true));
+      Plan<T>& D = *dryp[q];
+      require(D.n_init_allocs == n_init_allocs && D.steps().size() == NS,
+              "p2p_import: dry replay differs from the plan");
+      D.reset_state(nullptr);
+      T* fake = (T*)D.alloc((size_t)(lv[d.m].n / S) * d.ld * sizeof(T));
+      size_t si = 0;
+      for (const Step& st : D.steps()) {
+        D.run_step(st, fake, fake, nullptr);
+        D.comm_plan(st, xs_of[q][si], gs_of[q][si]);
+        si++;
+      }
+    }
+    auto map = [&](int q, const void* dp) -> const char* {
+      const uintptr_t a = (uintptr_t)dp;
+      const auto& da = dryp[q]->dry_allocs;
+      for (size_t k = 0; k < n_init_allocs; k++)
+        if (a >= da[k].first && a < da[k].first + da[k].second)
+          return base[q][k] + (a - da[k].first);
+      throw Error(ERR_INTERNAL, "p2p_import: transfer address outside the workspace");
+    };
+    p2p->recv_src.assign(NS, {});
+    p2p->gath_src.assign(NS, {});
+    for (size_t si = 0; si < NS; si++) {
+      std::vector<int> next(S, 0);  // receives from each peer so far in this step
+      for (const Xfer& x : xs_of[srank][si]) {
+        if (x.send) continue;
+        // the i-th send of peer x.peer to this rank
+        int i = next[x.peer]++, k = 0;
+        const Xfer* src = nullptr;
+        for (const Xfer& y : xs_of[x.peer][si])
+          if (y.send && y.peer == srank && k++ == i) {
+            src = &y;
+            break;
+          }
+        require(src && src->bytes == x.bytes && src->tag == x.tag,
+                "p2p_import: unmatched send / receive");
+        p2p->recv_src[si].push_back(map(x.peer, src->ptr));
+      }
+      for (size_t g = 0; g < gs_of[srank][si].size(); g++) {
+        std::vector<const char*> per(S);
+        for (int q = 0; q < S; q++) {
+          require(gs_of[q][si].size() == gs_of[srank][si].size(), "p2p_import: gathers differ");
+          per[q] = map(q, gs_of[q][si][g].base);
+        }
+        p2p->gath_src[si].push_back(per);
+      }
+    }
+    p2p->ready = true;
+  }
+  int p2p_status() override {
+    require(p2p, "p2p_status: not a peer-memory shard plan");
+    unsigned long long w[P2P_NWORDS];
+    check_cuda(cudaMemcpy(w, p2p->flags, sizeof w, cudaMemcpyDeviceToHost), "p2p status");
+    return (int)(w[P2P_ERR] & 0xffffffffu);
+  }
+  void comm_p2p(const Step& st, int si, cudaStream_t s) {
+    if (dry) return;
+    require(p2p->ready, "p2p: the peers' workspaces are not imported (fmgsr_shard_p2p_import)");
+    std::vector<Xfer> xs;
+    std::vector<Gather> gs;
+    comm_plan(st, xs, gs);
+    if (xs.empty() && gs.empty()) {
+      fixup(st, s);
+      return;
+    }
+    const unsigned long long nstep = steps().size() + 1, step = (unsigned long long)si + 1;
+    auto copy_base = [&](int which_wait, bool all) {
+      P2pCopy c;
+      c.nstep = nstep;
+      c.step = step;
+      c.timeout_ns = p2p->timeout_ns;
+      for (int q = 0; q < S; q++) {
+        if (q == srank) continue;
+        bool need = all;
+        for (const Xfer& x : xs) need = need || x.peer == q;
+        if (need) c.wait[c.nwait++] = p2p->peer_flags[q] + which_wait;
+      }
+      return c;
+    };
+    launch_p2p_signal(p2p->flags, P2P_READY, nstep, step, s);
+    n_launch++;
+    if (!xs.empty()) {
+      P2pCopy c = copy_base(P2P_READY, false);
+      size_t i = 0;
+      for (const Xfer& x : xs) {
+        if (x.send) continue;
+        require(c.n < P2P_MAXE, "p2p: too many receives in one step");
+        c.src[c.n] = p2p->recv_src[si][i++];
+        c.dst[c.n] = x.ptr;
+        c.bytes[c.n++] = x.bytes;
+      }
+      launch_p2p_wait_copy(c, p2p->flags, s);
+      n_launch++;
+    }
+    fixup(st, s);
+    if (!gs.empty()) {
+      launch_p2p_signal(p2p->flags, P2P_FIXED, nstep, step, s);
+      P2pCopy c = copy_base(P2P_FIXED, true);
+      for (size_t g = 0; g < gs.size(); g++)
+        for (int q = 0; q < S; q++) {
+          if (q == srank) continue;
+          require(c.n < P2P_MAXE, "p2p: too many gather chunks in one step");
+          c.src[c.n] = p2p->gath_src[si][g][q] + (size_t)q * gs[g].chunk;
+          c.dst[c.n] = gs[g].base + (size_t)q * gs[g].chunk;
+          c.bytes[c.n++] = gs[g].chunk;
+        }
+      launch_p2p_wait_copy(c, p2p->flags, s);
+      launch_p2p_signal(p2p->flags, P2P_DONE, nstep, step, s);
+      P2pCopy dn = copy_base(P2P_DONE, true);
+      launch_p2p_wait_copy(dn, p2p->flags, s);
+      n_launch += 4;
+    }
+  }
+
   void poison_all(cudaStream_t s) {
     if (dry || !(debug & FMGSR_DEBUG_POISON)) return;
     for (size_t k = 0; k < n_field_allocs; k++)
@@ -1273,10 +1498,16 @@ struct Plan : PlanBase {
   }
 
   void enqueue_coarse(const T* forcing, T* solution, cudaStream_t s) {
+    if (p2p && !dry) launch_p2p_epoch(p2p->flags, s);
+    int si = 0;
     for (const Step& st : steps()) {
       run_step(st, forcing, solution, s);
-      if (S > 1) comm_nccl(st, s);
+      if (S > 1) {
+        if (p2p) comm_p2p(st, si, s);
+        else comm_nccl(st, s);
+      }
       if (st.kind == ST_UP && st.l == st.t) poison_sr_below(st.t, s);
+      si++;
     }
   }
 
@@ -2018,6 +2249,46 @@ int fmgsr_shard_plan_create(const fmgsr_plan_desc* desc, int32_t shards, int32_t
       q->ncomm = comm;
     }
     *plan = p.release();
+  });
+}
+int fmgsr_shard_plan_create_p2p(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,
+                                void** plan) {
+  return guarded([&] {
+    require(desc && plan, "shard_plan_create_p2p: null argument");
+    validate_desc(*desc);
+    require(shards >= 2 && rank >= 0 && rank < shards, "shard_plan_create_p2p: bad rank / shards");
+    require(shards <= P2P_MAXW + 1, "shard_plan_create_p2p: at most 17 shards");
+    std::unique_ptr<PlanBase> p;
+    if (desc->dtype == 0) {
+      auto* q = new Plan<double>(*desc, shards, rank);
+      p.reset(q);
+      q->p2p_init();
+    } else {
+      auto* q = new Plan<float>(*desc, shards, rank);
+      p.reset(q);
+      q->p2p_init();
+    }
+    *plan = p.release();
+  });
+}
+int fmgsr_shard_p2p_export(void* plan, void* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    require(plan && len, "shard_p2p_export: null argument");
+    auto* p = static_cast<PlanBase*>(plan);
+    *len = (int64_t)p->p2p_export(nullptr, 0);
+    if (buf) p->p2p_export(buf, (size_t)cap);
+  });
+}
+int fmgsr_shard_p2p_import(void* plan, const void* all, int64_t per_rank) {
+  return guarded([&] {
+    require(plan && all && per_rank > 0, "shard_p2p_import: null argument");
+    static_cast<PlanBase*>(plan)->p2p_import(static_cast<const char*>(all), (size_t)per_rank);
+  });
+}
+int fmgsr_shard_p2p_status(void* plan, int32_t* err) {
+  return guarded([&] {
+    require(plan && err, "shard_p2p_status: null argument");
+    *err = static_cast<PlanBase*>(plan)->p2p_status();
   });
 }
 int fmgsr_shard_plan_create_local(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,

@@ -265,6 +265,22 @@ template <typename T> void launch_restrict_tau(const T* u, const T* f, T* uH_out
 template <typename T> void launch_direct_solve_nl(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_fas_correct(const T* u, const T* uH, T* out, i64 nf, i64 ld, int B, cudaStream_t s);
 template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, int B, cudaStream_t s, T* workspace = nullptr);
+// peer-memory transport of the sharded plan (kernels_p2p.cu): per-rank
+// counter words and one step's pulls
+enum { P2P_READY = 0, P2P_FIXED = 1, P2P_DONE = 2, P2P_EPOCH = 3, P2P_ERR = 4, P2P_NWORDS = 8 };
+constexpr int P2P_MAXE = 40, P2P_MAXW = 16;
+struct P2pCopy {
+  int n = 0, nwait = 0;
+  unsigned long long nstep = 0, step = 0, timeout_ns = 0;
+  const unsigned long long* wait[P2P_MAXW];
+  const void* src[P2P_MAXE];
+  void* dst[P2P_MAXE];
+  unsigned long long bytes[P2P_MAXE];
+};
+void launch_p2p_epoch(unsigned long long* flags, cudaStream_t s);
+void launch_p2p_signal(unsigned long long* flags, int which, unsigned long long nstep,
+                       unsigned long long step, cudaStream_t s);
+void launch_p2p_wait_copy(const P2pCopy& c, unsigned long long* flags, cudaStream_t s);
 template <typename T> void launch_banded_lu_solve(const T* f, T* u, i64 n, i64 ld, int B, T* workspace, int* bad, cudaStream_t s);
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);
 template <typename T> void launch_kaczmarz_sweep(T* u, const T* uc, i64 n, i64 ld, int B, i64 start, i64 stop, double proj_diag, cudaStream_t s);

@@ -1,0 +1,115 @@
+// kernels_p2p.cu -- peer-memory transport of the patch-slab sharded plan.
+//
+// The NCCL transport (capi.cu comm_nccl) turns each exchange of the sharded
+// schedule into a grouped ncclSend / ncclRecv round.  This transport needs no
+// collective library: every rank maps its peers' plan workspaces (CUDA IPC
+// handles, NVLink peer access between GPUs) and PULLS what it needs -- the
+// neighbours' boundary rows and tau edge records, every rank's chunk of the
+// replication-cutoff level -- straight into its own halo / inbox / replicated
+// arrays.  All writes are local; only reads cross the link, so no rank ever
+// writes into memory a peer is still reading.  Ordering is three monotonic
+// per-rank counters in device memory (READY after a rank's visit, FIXED after
+// its slab-edge fix-ups, DONE after its gather), published with
+// st.release.sys and polled with ld.acquire.sys; a step's value is
+// epoch * steps_per_solve + step, and the epoch advances once per solve on
+// the device (so captured CUDA graphs replay unchanged).
+#include <cstdint>
+
+#include "fmgsr_internal.h"
+
+namespace fmgsr {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_p2p_epoch(unsigned long long* flags) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) flags[P2P_EPOCH] += 1;
+}
+
+__global__ void k_p2p_signal(unsigned long long* flags, int which, unsigned long long nstep,
+                             unsigned long long step) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();  // this rank's earlier kernels' writes, then the counter
+    st_release_sys(flags + which, flags[P2P_EPOCH] * nstep + step);
+  }
+}
+
+// Thread 0 of every CTA polls the listed peer counters until they reach this
+// step's value (bounded: past the timeout the error word is set and nothing is
+// copied, so a broken peer cannot hang the GPU); then the CTA copies its share
+// of every (remote source, local destination) pair, 16 bytes per thread and
+// step, through L2 only (ld.global.cg: a peer's rows are never served stale
+// from L1).
+__global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const unsigned long long v = flags[P2P_EPOCH] * c.nstep + c.step;
+    int good = 1;
+    for (int k = 0; k < c.nwait && good; k++) {
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys(c.wait[k]) < v) {
+        __nanosleep(256);
+        if (globaltimer_ns() - t0 > c.timeout_ns) {
+          good = 0;
+          atomicExch(reinterpret_cast<unsigned int*>(flags + P2P_ERR), 1u);
+          break;
+        }
+      }
+    }
+    ok = good;
+  }
+  __syncthreads();  // orders every thread's loads below after thread 0's acquire
+  if (!ok) return;
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  for (int e = 0; e < c.n; e++) {
+    const uint4* s = reinterpret_cast<const uint4*>(c.src[e]);
+    uint4* d = reinterpret_cast<uint4*>(c.dst[e]);
+    const unsigned long long w = c.bytes[e] >> 4;
+    for (unsigned long long i = tid; i < w; i += nth) d[i] = __ldcg(s + i);
+  }
+}
+
+}  // namespace
+
+void launch_p2p_epoch(unsigned long long* flags, cudaStream_t s) {
+  k_p2p_epoch<<<1, 32, 0, s>>>(flags);
+  check_launch("p2p_epoch");
+}
+void launch_p2p_signal(unsigned long long* flags, int which, unsigned long long nstep,
+                       unsigned long long step, cudaStream_t s) {
+  k_p2p_signal<<<1, 32, 0, s>>>(flags, which, nstep, step);
+  check_launch("p2p_signal");
+}
+void launch_p2p_wait_copy(const P2pCopy& c, unsigned long long* flags, cudaStream_t s) {
+  require(c.n >= 0 && c.n <= P2P_MAXE && c.nwait >= 0 && c.nwait <= P2P_MAXW,
+          "p2p: too many transfers in one step");
+  unsigned long long total = 0;
+  for (int e = 0; e < c.n; e++) {
+    require(c.bytes[e] % 16 == 0 && ((uintptr_t)c.src[e] & 15) == 0 &&
+                ((uintptr_t)c.dst[e] & 15) == 0,
+            "p2p: transfers must be 16-byte aligned multiples of 16 bytes");
+    total += c.bytes[e];
+  }
+  // ~64 KB per CTA, at most one CTA per SM (every CTA polls the counters)
+  unsigned long long blocks = (total + 65535) / 65536;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148) blocks = 148;
+  k_p2p_wait_copy<<<(unsigned)blocks, 256, 0, s>>>(c, flags);
+  check_launch("p2p_wait_copy");
+}
+
+}  // namespace fmgsr

@@ -10,8 +10,10 @@ by every shard.  Two drivers run the same sharded schedule:
   stream, transfers as device copies -- bit-identical to the unsharded plan
   (``tests/test_gpu_shard.py``);
 * ``ShardedPlan``: one shard per GPU (one process per GPU, torchrun), halos
-  and edge records over NCCL send/recv, the cutoff level over NCCL all-gather,
-  all captured in the plan's CUDA graph.
+  and edge records over NCCL send/recv and the cutoff level over NCCL
+  all-gather -- or, ``transport="p2p"``, pulled straight from the peers'
+  workspaces over peer memory with device-side counters -- all captured in
+  the plan's CUDA graph.
 """
 
 from __future__ import annotations
@@ -90,25 +92,69 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _allgather_bytes(blob: bytes) -> list[bytes]:
+    """Every rank's blob in rank order over the default torch.distributed group."""
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, blob)
+    return out
+
+
 class ShardedPlan:
-    """This rank's shard of one problem, one GPU per rank, exchanges over NCCL.
+    """This rank's shard of one problem, one GPU per rank.
 
-    ``uid`` is the 128-byte id from ``nccl_unique_id()`` on rank 0, broadcast
-    to every rank (e.g. with torch.distributed).  ``solve`` takes and returns
-    the rank's slab: (2**m / shards, B) rows [c0, c1) of the global arrays."""
+    ``transport="nccl"``: halos, edge records and the cutoff gather over NCCL
+    send / recv / all-gather; ``uid`` is the 128-byte id from
+    ``nccl_unique_id()`` on rank 0, broadcast to every rank (e.g. with
+    torch.distributed).
+    ``transport="p2p"``: no collective library -- every rank maps its peers'
+    plan workspaces (CUDA IPC, NVLink peer access) and pulls what it needs with
+    device-side release / acquire counters (fmgsr_shard_plan_create_p2p);
+    ``exchange(blob) -> [blob of rank 0, ..., blob of rank S-1]`` is any host
+    all-gather (default: torch.distributed.all_gather_object), used once.  It
+    also runs with several ranks on ONE GPU (the one-GPU multi-process tests).
+    ``solve`` takes and returns the rank's slab: (2**m / shards, B) rows
+    [c0, c1) of the global arrays."""
 
-    def __init__(self, cfg, B: int, shards: int, rank: int, uid: bytes, dtype=torch.float64,
-                 coarse: int = -1, use_graph: bool = True):
+    def __init__(self, cfg, B: int, shards: int, rank: int, uid: bytes | None = None,
+                 dtype=torch.float64, coarse: int = -1, use_graph: bool = True,
+                 transport: str = "nccl", exchange=None):
         N.require_cuda()
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.key = key_from_config(cfg, B, dtype, use_graph=use_graph, coarse=coarse)
         d = _desc(self.key)
-        idbuf = (C.c_uint8 * 128).from_buffer_copy(uid)
         h = C.c_void_p()
-        N.check(N.lib().fmgsr_shard_plan_create(C.byref(d), int(shards), int(rank), idbuf,
-                                                C.byref(h)), "shard_plan_create")
+        if transport == "nccl":
+            if uid is None:
+                raise ValueError("the NCCL transport needs the rank-0 unique id (uid)")
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            N.check(N.lib().fmgsr_shard_plan_create(C.byref(d), int(shards), int(rank), idbuf,
+                                                    C.byref(h)), "shard_plan_create")
+        else:
+            N.check(N.lib().fmgsr_shard_plan_create_p2p(C.byref(d), int(shards), int(rank),
+                                                        C.byref(h)), "shard_plan_create_p2p")
         self._h = h
-        self.shards, self.rank = shards, rank
+        self.shards, self.rank, self.transport = shards, rank, transport
         self.rows = 2 ** self.key.m // shards
+        if transport == "p2p":
+            n = C.c_int64()
+            N.check(N.lib().fmgsr_shard_p2p_export(h, None, 0, C.byref(n)), "shard_p2p_export")
+            buf = (C.c_uint8 * n.value)()
+            N.check(N.lib().fmgsr_shard_p2p_export(h, buf, n.value, C.byref(n)),
+                    "shard_p2p_export")
+            blobs = (exchange or _allgather_bytes)(bytes(buf))
+            if len(blobs) != shards or any(len(b) != n.value for b in blobs):
+                raise ValueError("p2p exchange: expected one blob per rank of equal size")
+            allb = (C.c_uint8 * (n.value * shards)).from_buffer_copy(b"".join(blobs))
+            N.check(N.lib().fmgsr_shard_p2p_import(h, allb, n.value), "shard_p2p_import")
+
+    def status(self) -> int:
+        """p2p transport: synchronise and return 0, or non-zero if a peer wait timed out."""
+        err = C.c_int32()
+        N.check(N.lib().fmgsr_shard_p2p_status(self._h, C.byref(err)), "shard_p2p_status")
+        return err.value
 
     def __del__(self):
         h = getattr(self, "_h", None)
