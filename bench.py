@@ -14,8 +14,11 @@ and the one BASELINE.json names for the 1/2/4/8-GPU sweep.
   configs[1]) measured in the same process.
 * N > 1 (one process per GPU, torchrun; ``--gpus N`` without torchrun spawns
   it): the ONE config-4 problem is split into N patch slabs:
-  strong scaling, halos and tau edge records over NCCL send/recv, the
-  replication cutoff over NCCL all-gather, levels below it replicated.  The
+  strong scaling, halos, tau edge records and the replication-cutoff level
+  pulled from the peers' workspaces over peer memory (``--transport p2p``,
+  default) or moved by NCCL send/recv + all-gather (``--transport nccl``),
+  levels below the cutoff replicated.  The sharded result is compared bit for
+  bit with the unsharded plan on the same forcing (``sharded_bit_exact_...``).  The
   independent-RHS-batch split (every rank its own config-4 batch, weak
   scaling, no data-path collective) is reported beside it as a control.
   ``--shard rhs`` makes the control the headline instead.
@@ -221,12 +224,18 @@ def run_reference(args, w):
     return 0
 
 
-def workload_config(name, w, world, shard="patches"):
+TRANSPORTS = {
+    "p2p": "halos / tau edge records / cutoff-level chunks pulled from the peers' "
+           "workspaces over peer memory (CUDA IPC, NVLink), device-side counters",
+    "nccl": "NCCL send/recv halos / tau edge records, NCCL all-gather at the cutoff",
+}
+
+
+def workload_config(name, w, world, shard="patches", transport="p2p"):
     esz = 8 if w["dtype"] == "f64" else 4
     sharded = world > 1 and shard == "patches"
-    par = (f"patch slabs x{world} of one problem (NCCL halos / tau edge records, "
-           "all-gather at the replication cutoff, coarse levels replicated)" if sharded
-           else f"dp{world} (independent RHS batches per GPU)")
+    par = (f"patch slabs x{world} of one problem ({TRANSPORTS[transport]}; coarse levels "
+           "replicated)" if sharded else f"dp{world} (independent RHS batches per GPU)")
     return {
         "workload": f"{name}: 1D {'-u\'\'+u^3=f' if w.get('nonlinear') else 'Poisson'} "
                     f"FMG-FAS-SR, N=2^{w['m']} fine cells, m0={w['m0']}, "
@@ -623,8 +632,11 @@ def run_gpu_sharded(args, w):
     # send has its matching receive, tests/test_shard_schedule.py.)
     plan, fs, sol, err = None, None, None, None
     try:
-        uid = broadcast_uid(nccl_unique_id() if rank == 0 else None, rank, device=cdev)
-        plan = ShardedPlan(cfg, B, world, rank, uid, dtype)
+        if args.transport == "nccl":
+            uid = broadcast_uid(nccl_unique_id() if rank == 0 else None, rank, device=cdev)
+            plan = ShardedPlan(cfg, B, world, rank, uid, dtype)
+        else:
+            plan = ShardedPlan(cfg, B, world, rank, dtype=dtype, transport="p2p")
         f = _forcing(fm, w, dtype, 0)  # the one problem (same seed on every rank)
         fs = f[c0:c1].contiguous()
         del f
@@ -660,6 +672,7 @@ def run_gpu_sharded(args, w):
     e2e_ms = _timed(e2e_step, args.steps, world, stream, dist.barrier)
     info = plan.info()
     plan.solve(fs, sol)  # the timed solves' result, kept for the parity check
+    xerr = plan.status() if args.transport == "p2p" else 0  # a peer wait timed out?
     sol_keep = sol
     del hf, hs, dfi, fs, plan
     torch.cuda.empty_cache()
@@ -700,7 +713,7 @@ def run_gpu_sharded(args, w):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype_label(w), "data": "synthetic (seeded Fourier RHS, SURVEY 8(d))",
-            "config": workload_config(args.workload, w, world, "patches"),
+            "config": workload_config(args.workload, w, world, "patches", args.transport),
             "roofline": {"bound": "hbm", "achieved": alg / world / (ms_step / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s",
                          "frac": alg / world / (ms_step / 1e3) / 1e9 / peak, "traffic": None,
@@ -715,6 +728,7 @@ def run_gpu_sharded(args, w):
             "clocks": clocks, "cpu_baseline": None,
             "control_rhs_batch": control,
             "sharded_bit_exact_vs_unsharded": exact,
+            "transport": args.transport, "transport_timeouts": xerr,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -735,6 +749,8 @@ def parse_args(argv=None):
                     help="skip the config-2 line (N=1) / the RHS-batch control (N>1)")
     ap.add_argument("--e2e-chunks", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="exchanges of the patch-slab split: peer-memory pulls (default) or NCCL")
     ap.add_argument("--shard", default="patches", choices=["rhs", "patches"],
                     help="multi-GPU split: patch slabs of one problem (strong, SURVEY 8(e), "
                          "default) or independent RHS batches per rank (weak control)")

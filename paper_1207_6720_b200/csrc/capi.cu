@@ -1417,10 +1417,9 @@ struct Plan : PlanBase {
       }
       return c;
     };
-    launch_p2p_signal(p2p->flags, P2P_READY, nstep, step, s);
-    n_launch++;
     if (!xs.empty()) {
       P2pCopy c = copy_base(P2P_READY, false);
+      c.signal = P2P_READY;
       size_t i = 0;
       for (const Xfer& x : xs) {
         if (x.send) continue;
@@ -1434,8 +1433,8 @@ struct Plan : PlanBase {
     }
     fixup(st, s);
     if (!gs.empty()) {
-      launch_p2p_signal(p2p->flags, P2P_FIXED, nstep, step, s);
       P2pCopy c = copy_base(P2P_FIXED, true);
+      c.signal = P2P_FIXED;
       for (size_t g = 0; g < gs.size(); g++)
         for (int q = 0; q < S; q++) {
           if (q == srank) continue;
@@ -1445,10 +1444,10 @@ struct Plan : PlanBase {
           c.bytes[c.n++] = gs[g].chunk;
         }
       launch_p2p_wait_copy(c, p2p->flags, s);
-      launch_p2p_signal(p2p->flags, P2P_DONE, nstep, step, s);
       P2pCopy dn = copy_base(P2P_DONE, true);
+      dn.signal = P2P_DONE;
       launch_p2p_wait_copy(dn, p2p->flags, s);
-      n_launch += 4;
+      n_launch += 2;
     }
   }
 

@@ -39,16 +39,9 @@ __global__ void k_p2p_epoch(unsigned long long* flags) {
   if (blockIdx.x == 0 && threadIdx.x == 0) flags[P2P_EPOCH] += 1;
 }
 
-__global__ void k_p2p_signal(unsigned long long* flags, int which, unsigned long long nstep,
-                             unsigned long long step) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    __threadfence_system();  // this rank's earlier kernels' writes, then the counter
-    st_release_sys(flags + which, flags[P2P_EPOCH] * nstep + step);
-  }
-}
-
-// Thread 0 of every CTA polls the listed peer counters until they reach this
-// step's value (bounded: past the timeout the error word is set and nothing is
+// CTA 0 first publishes this rank's counter c.signal (if >= 0); thread 0 of
+// every CTA then polls the listed peer counters until they reach this step's
+// value (bounded: past the timeout the error word is set and nothing is
 // copied, so a broken peer cannot hang the GPU); then the CTA copies its share
 // of every (remote source, local destination) pair, 16 bytes per thread and
 // step, through L2 only (ld.global.cg: a peer's rows are never served stale
@@ -57,6 +50,12 @@ __global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
   __shared__ int ok;
   if (threadIdx.x == 0) {
     const unsigned long long v = flags[P2P_EPOCH] * c.nstep + c.step;
+    // publish this rank's counter first (this launch follows the step's
+    // kernels in stream order, so their writes are complete), then wait
+    if (c.signal >= 0 && blockIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(flags + c.signal, v);
+    }
     int good = 1;
     for (int k = 0; k < c.nwait && good; k++) {
       const unsigned long long t0 = globaltimer_ns();
@@ -88,11 +87,6 @@ __global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
 void launch_p2p_epoch(unsigned long long* flags, cudaStream_t s) {
   k_p2p_epoch<<<1, 32, 0, s>>>(flags);
   check_launch("p2p_epoch");
-}
-void launch_p2p_signal(unsigned long long* flags, int which, unsigned long long nstep,
-                       unsigned long long step, cudaStream_t s) {
-  k_p2p_signal<<<1, 32, 0, s>>>(flags, which, nstep, step);
-  check_launch("p2p_signal");
 }
 void launch_p2p_wait_copy(const P2pCopy& c, unsigned long long* flags, cudaStream_t s) {
   require(c.n >= 0 && c.n <= P2P_MAXE && c.nwait >= 0 && c.nwait <= P2P_MAXW,
