@@ -1303,13 +1303,26 @@ struct Plan : PlanBase {
   void p2p_import(const char* all, size_t per_rank) override {
     require(p2p && !p2p->ready, "p2p_import: not a fresh peer-memory shard plan");
     require(per_rank >= p2p_blob_bytes(n_init_allocs), "p2p_import: blob too small");
+    // FMGSR_P2P_SELF_PROBE=1 (timing probe on one GPU, results are not a
+    // solve): every "peer" is this rank itself -- the S blobs may all be this
+    // rank's -- so each wait is met by this rank's own counter and each pull
+    // reads this rank's memory at the peer's offsets: the transport's launch,
+    // fence, poll and copy cost without a second GPU
+    const char* sp = getenv("FMGSR_P2P_SELF_PROBE");
+    const bool self_probe = sp && sp[0] == '1';
     // every rank's allocation bases (user pointers) and counter words
     std::vector<std::vector<char*>> base(S);
     p2p->peer_flags.assign(S, nullptr);
     for (int q = 0; q < S; q++) {
       const P2pBlob* b = reinterpret_cast<const P2pBlob*>(all + (size_t)q * per_rank);
-      require(b->magic == 0x46474d5350325031ull && b->rank == (unsigned long long)q,
+      require(b->magic == 0x46474d5350325031ull &&
+                  (self_probe || b->rank == (unsigned long long)q),
               "p2p_import: blob of rank " + std::to_string(q) + " is not a shard plan export");
+      if (self_probe && q != srank) {
+        for (size_t k = 0; k < n_init_allocs; k++) base[q].push_back((char*)alloc_user[k]);
+        p2p->peer_flags[q] = p2p->flags;
+        continue;
+      }
       require(b->n_alloc == n_init_allocs && b->guard == (guards ? GUARD : 0),
               "p2p_import: peer plans differ (descriptor, shard count or FMGSR_GUARDS)");
       if (q == srank) {
@@ -1420,18 +1433,50 @@ struct Plan : PlanBase {
     if (!xs.empty()) {
       P2pCopy c = copy_base(P2P_READY, false);
       c.signal = P2P_READY;
+      // this step's slab-edge fix-ups (as fixup()), folded into the kernel
+      if ((st.kind == ST_TOP || st.kind == ST_DOWN) && sharded(st.l)) {
+        const int l = st.l;
+        const i64 Bp = ((d.B + 31) / 32) * 32, slot = 5 * Bp;
+        auto add_fix = [&](const T* L, const T* R, i64 sb) {
+          P2pFix& x = c.fix[c.nfix++];
+          x.L = L;
+          x.R = R;
+          x.fH = lv[l - 1].f;
+          x.s = sb;
+          x.nf = lv[l].n;
+          x.ld = d.ld;
+          x.ldE = Bp;
+          x.B = (int)d.B;
+        };
+        if (c0(l) > 0) add_fix(ib[l], ob[l], c0(l));
+        if (c1(l) < lv[l].n) add_fix(ob[l] + slot, ib[l] + slot, c1(l));
+      }
+      auto overlaps = [](const void* a, size_t na, const void* b, size_t nb) {
+        const char *x = (const char*)a, *y = (const char*)b;
+        return x < y + nb && y < x + na;
+      };
       size_t i = 0;
       for (const Xfer& x : xs) {
         if (x.send) continue;
         require(c.n < P2P_MAXE, "p2p: too many receives in one step");
         c.src[c.n] = p2p->recv_src[si][i++];
         c.dst[c.n] = x.ptr;
-        c.bytes[c.n++] = x.bytes;
+        c.bytes[c.n] = x.bytes;
+        bool mine = false;  // read or overwritten by a fix-up: CTA 0 copies it first
+        for (int k = 0; k < c.nfix; k++) {
+          const P2pFix& f = c.fix[k];
+          const size_t rec = (size_t)5 * f.ldE * sizeof(T);
+          const T* cells = (const T*)f.fH + (f.s / 2 - 1) * f.ld;
+          mine = mine || overlaps(x.ptr, x.bytes, f.L, rec) || overlaps(x.ptr, x.bytes, f.R, rec) ||
+                 overlaps(x.ptr, x.bytes, cells, (size_t)(f.ld + f.B) * sizeof(T));
+        }
+        c.cta0[c.n++] = mine;
       }
-      launch_p2p_wait_copy(c, p2p->flags, s);
+      launch_p2p_wait_copy<T>(c, p2p->flags, s);
       n_launch++;
+    } else {
+      fixup(st, s);
     }
-    fixup(st, s);
     if (!gs.empty()) {
       P2pCopy c = copy_base(P2P_FIXED, true);
       c.signal = P2P_FIXED;
@@ -1443,10 +1488,11 @@ struct Plan : PlanBase {
           c.dst[c.n] = gs[g].base + (size_t)q * gs[g].chunk;
           c.bytes[c.n++] = gs[g].chunk;
         }
-      launch_p2p_wait_copy(c, p2p->flags, s);
+      for (int e = 0; e < c.n; e++) c.cta0[e] = 0;
+      launch_p2p_wait_copy<T>(c, p2p->flags, s);
       P2pCopy dn = copy_base(P2P_DONE, true);
       dn.signal = P2P_DONE;
-      launch_p2p_wait_copy(dn, p2p->flags, s);
+      launch_p2p_wait_copy<T>(dn, p2p->flags, s);
       n_launch += 2;
     }
   }

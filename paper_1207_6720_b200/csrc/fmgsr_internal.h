@@ -269,15 +269,28 @@ template <typename T> void launch_direct_solve(const T* f, T* u, i64 n, i64 ld, 
 // counter words and one step's pulls
 enum { P2P_READY = 0, P2P_FIXED = 1, P2P_DONE = 2, P2P_EPOCH = 3, P2P_ERR = 4, P2P_NWORDS = 8 };
 constexpr int P2P_MAXE = 40, P2P_MAXW = 16;
+// A slab-edge fix-up folded into the exchange kernel: coarse cells s/2-1, s/2
+// of f_H from the left (L) and right (R) 5-value edge records (k_edge_fix).
+struct P2pFix {
+  const void* L;
+  const void* R;
+  void* fH;
+  i64 s, nf, ld, ldE;
+  int B;
+};
 struct P2pCopy {
   int n = 0, nwait = 0, signal = -1;  // signal: counter word to publish first (-1: none)
+  int nfix = 0;
   unsigned long long nstep = 0, step = 0, timeout_ns = 0;
   const unsigned long long* wait[P2P_MAXW];
   const void* src[P2P_MAXE];
   void* dst[P2P_MAXE];
   unsigned long long bytes[P2P_MAXE];
+  unsigned char cta0[P2P_MAXE];  // copied by CTA 0 alone (fix-up inputs and outputs)
+  P2pFix fix[2];
 };
 void launch_p2p_epoch(unsigned long long* flags, cudaStream_t s);
+template <typename T>
 void launch_p2p_wait_copy(const P2pCopy& c, unsigned long long* flags, cudaStream_t s);
 template <typename T> void launch_banded_lu_solve(const T* f, T* u, i64 n, i64 ld, int B, T* workspace, int* bad, cudaStream_t s);
 template <typename T> void launch_gs_sweep(T* u, const T* f, i64 n, i64 ld, int B, double inv_h2, i64 start, i64 stop, bool forward, double omega, cudaStream_t s);

@@ -15,6 +15,7 @@
 // the device (so captured CUDA graphs replay unchanged).
 #include <cstdint>
 
+#include "fmgsr_device.cuh"
 #include "fmgsr_internal.h"
 
 namespace fmgsr {
@@ -42,10 +43,14 @@ __global__ void k_p2p_epoch(unsigned long long* flags) {
 // CTA 0 first publishes this rank's counter c.signal (if >= 0); thread 0 of
 // every CTA then polls the listed peer counters until they reach this step's
 // value (bounded: past the timeout the error word is set and nothing is
-// copied, so a broken peer cannot hang the GPU); then the CTA copies its share
-// of every (remote source, local destination) pair, 16 bytes per thread and
-// step, through L2 only (ld.global.cg: a peer's rows are never served stale
-// from L1).
+// copied, so a broken peer cannot hang the GPU); then the CTAs copy every
+// (remote source, local destination) pair, 16 bytes per thread and load,
+// through L2 only (ld.global.cg: a peer's rows are never served stale from
+// L1).  The slab-edge fix-ups of the step (c.fix) run in CTA 0 after it has
+// copied, by itself, every entry they read or overwrite (the edge records,
+// the halo rows of f_H holding the neighbour's boundary cell) -- one launch
+// per exchange round instead of three.
+template <typename T>
 __global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
   __shared__ int ok;
   if (threadIdx.x == 0) {
@@ -60,7 +65,7 @@ __global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
     for (int k = 0; k < c.nwait && good; k++) {
       const unsigned long long t0 = globaltimer_ns();
       while (ld_acquire_sys(c.wait[k]) < v) {
-        __nanosleep(256);
+        __nanosleep(32);
         if (globaltimer_ns() - t0 > c.timeout_ns) {
           good = 0;
           atomicExch(reinterpret_cast<unsigned int*>(flags + P2P_ERR), 1u);
@@ -72,13 +77,53 @@ __global__ void k_p2p_wait_copy(P2pCopy c, unsigned long long* flags) {
   }
   __syncthreads();  // orders every thread's loads below after thread 0's acquire
   if (!ok) return;
-  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  auto copy = [](const void* src, void* dst, unsigned long long bytes, unsigned long long tid,
+                 unsigned long long nth) {
+    // four independent 16-byte loads in flight per thread before their stores:
+    // the copy is latency-bound (a link round trip per pass)
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const unsigned long long w = bytes >> 4;
+    for (unsigned long long i = tid; i < w; i += 4 * nth) {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (i + k * nth < w) v[k] = __ldcg(s + i + k * nth);
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (i + k * nth < w) d[i + k * nth] = v[k];
+    }
+  };
+  const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long gth = (unsigned long long)gridDim.x * blockDim.x;
   for (int e = 0; e < c.n; e++) {
-    const uint4* s = reinterpret_cast<const uint4*>(c.src[e]);
-    uint4* d = reinterpret_cast<uint4*>(c.dst[e]);
-    const unsigned long long w = c.bytes[e] >> 4;
-    for (unsigned long long i = tid; i < w; i += nth) d[i] = __ldcg(s + i);
+    if (c.cta0[e]) {
+      if (blockIdx.x == 0) copy(c.src[e], c.dst[e], c.bytes[e], threadIdx.x, blockDim.x);
+    } else {
+      copy(c.src[e], c.dst[e], c.bytes[e], gtid, gth);
+    }
+  }
+  if (blockIdx.x != 0 || c.nfix == 0) return;
+  __syncthreads();
+  for (int k = 0; k < c.nfix; k++) {
+    const P2pFix& x = c.fix[k];
+    const T* L = static_cast<const T*>(x.L);
+    const T* R = static_cast<const T*>(x.R);
+    T* fH = static_cast<T*>(x.fH);
+    const int lv = level_of(x.nf);
+    const T ih = (T)pow4(lv), iH = (T)pow4(lv - 1);
+    for (int r = threadIdx.x; r < x.B; r += blockDim.x) {
+      T Lr[5], Rr[5];
+#pragma unroll
+      for (int q = 0; q < 5; q++) {
+        Lr[q] = L[q * x.ldE + r];
+        Rr[q] = R[q * x.ldE + r];
+      }
+      T fL, fR;
+      edge_finish(Lr, Rr, ih, iH, fL, fR);
+      fH[(x.s / 2 - 1) * x.ld + r] = fL;
+      fH[(x.s / 2) * x.ld + r] = fR;
+    }
   }
 }
 
@@ -88,22 +133,27 @@ void launch_p2p_epoch(unsigned long long* flags, cudaStream_t s) {
   k_p2p_epoch<<<1, 32, 0, s>>>(flags);
   check_launch("p2p_epoch");
 }
+template <typename T>
 void launch_p2p_wait_copy(const P2pCopy& c, unsigned long long* flags, cudaStream_t s) {
-  require(c.n >= 0 && c.n <= P2P_MAXE && c.nwait >= 0 && c.nwait <= P2P_MAXW,
+  require(c.n >= 0 && c.n <= P2P_MAXE && c.nwait >= 0 && c.nwait <= P2P_MAXW &&
+              c.nfix >= 0 && c.nfix <= 2,
           "p2p: too many transfers in one step");
   unsigned long long total = 0;
   for (int e = 0; e < c.n; e++) {
     require(c.bytes[e] % 16 == 0 && ((uintptr_t)c.src[e] & 15) == 0 &&
                 ((uintptr_t)c.dst[e] & 15) == 0,
             "p2p: transfers must be 16-byte aligned multiples of 16 bytes");
-    total += c.bytes[e];
+    if (!c.cta0[e]) total += c.bytes[e];
   }
-  // ~64 KB per CTA, at most one CTA per SM (every CTA polls the counters)
-  unsigned long long blocks = (total + 65535) / 65536;
+  // ~16 KB per CTA (one pass of four loads per thread), at most one CTA per SM
+  // (every CTA polls the counters)
+  unsigned long long blocks = (total + 16383) / 16384;
   if (blocks < 1) blocks = 1;
   if (blocks > 148) blocks = 148;
-  k_p2p_wait_copy<<<(unsigned)blocks, 256, 0, s>>>(c, flags);
+  k_p2p_wait_copy<T><<<(unsigned)blocks, 256, 0, s>>>(c, flags);
   check_launch("p2p_wait_copy");
 }
+template void launch_p2p_wait_copy<double>(const P2pCopy&, unsigned long long*, cudaStream_t);
+template void launch_p2p_wait_copy<float>(const P2pCopy&, unsigned long long*, cudaStream_t);
 
 }  // namespace fmgsr

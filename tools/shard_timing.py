@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_1207_6720_b200 as fm  # noqa: E402
-from paper_1207_6720_b200.shard import LocalShardPlan, comm_schedule  # noqa: E402
+from paper_1207_6720_b200.shard import LocalShardPlan, ShardedPlan, comm_schedule  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="config4")
@@ -64,16 +64,34 @@ for S in a.shards:
         per[r] = timeit(lambda: p.solve(fs, out), a.reps)
         del p, fs, out
         torch.cuda.empty_cache()
+    # the same shard with the peer-memory transport mapped onto itself
+    # (FMGSR_P2P_SELF_PROBE): its exchange kernels' cost -- launch, fence,
+    # counter poll, copy from HBM instead of over NVLink -- on top of T_S
+    os.environ["FMGSR_P2P_SELF_PROBE"] = "1"
+    r = S // 2
+    p = ShardedPlan(cfg, B, S, r, dtype=torch.float64, transport="p2p",
+                    exchange=lambda blob: [blob] * S)
+    fs = f[r * rows:(r + 1) * rows].contiguous()
+    out = torch.empty_like(fs)
+    t_p2p = timeit(lambda: p.solve(fs, out), a.reps)
+    del p, fs, out
+    os.environ.pop("FMGSR_P2P_SELF_PROBE")
+    torch.cuda.empty_cache()
     recs, cut, halo = comm_schedule(cfg, B, S, S // 2)
     rounds = len({x["step"] for x in recs if x["kind"] in ("send", "recv")})
     gathers = sum(1 for x in recs if x["kind"] == "allgather")
     tS = max(per.values())
     eff = t1 / (S * tS)
+    t_x = t_p2p - per[r]  # transport overhead of the middle shard
+    eff_x = t1 / (S * (tS + t_x))
     res["shards"][S] = {"ms_per_rank": per, "t_shard_ms": tS, "cutoff": cut, "halo_rows": halo,
                         "p2p_rounds": rounds, "allgathers": gathers,
-                        "predicted_efficiency_before_transport": eff}
+                        "predicted_efficiency_before_transport": eff,
+                        "p2p_self_probe_ms": t_p2p, "p2p_overhead_ms": t_x,
+                        "predicted_efficiency_with_p2p_overhead": eff_x}
     print(f"  S={S}: cutoff L_r={cut}, per-shard ms {dict((k, round(v, 3)) for k, v in per.items())}"
-          f" -> T1/(S*T_S) = {eff:.3f} before transport ({rounds} p2p rounds, {gathers} all-gathers)")
+          f" -> T1/(S*T_S) = {eff:.3f} before transport ({rounds} exchange rounds, {gathers} "
+          f"gathers); p2p transport kernels +{t_x:.3f} ms (self-mapped probe) -> {eff_x:.3f}")
 if a.json:
     with open(a.json, "w") as fh:
         json.dump(res, fh, indent=1)
