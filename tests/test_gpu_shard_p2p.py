@@ -14,10 +14,12 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-CASES = [  # m, P, b, n_sr, B, shards, coarse
-    (12, 64, 4, 1, 64, 2, -1),
-    (13, 256, 8, 1, 64, 4, 6),   # config-4 style buffer, cutoff forced low: many rounds
-    (12, 32, 3, 0, 96, 2, 6),    # odd buffer, no SR, B not a multiple of 64
+CASES = [  # m, P, b, n_sr, B, shards, coarse, dtype
+    (12, 64, 4, 1, 64, 2, -1, "f64"),
+    (13, 256, 8, 1, 64, 4, 6, "f64"),   # config-4 style buffer, cutoff forced low: many rounds
+    (12, 32, 3, 0, 96, 2, 6, "f64"),    # odd buffer, no SR, B not a multiple of 64
+    (13, 256, 8, 2, 64, 8, 6, "f64"),   # 8 ranks, two SR levels
+    (12, 64, 4, 1, 64, 4, 6, "f32"),    # fp32 fields
 ]
 
 
@@ -38,11 +40,12 @@ def _rank_main(rank, world, port, case, q):
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
-        m, P, b, n_sr, B, S, coarse = case
+        m, P, b, n_sr, B, S, coarse, dt = case
+        dtype = torch.float64 if dt == "f64" else torch.float32
         cfg = _cfg(fm, m, P, b, n_sr)
-        f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + S))
+        f, _ = fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + S), dtype)
         c0, c1 = slab(2 ** m, S, rank)
-        plan = ShardedPlan(cfg, B, S, rank, coarse=coarse, transport="p2p")
+        plan = ShardedPlan(cfg, B, S, rank, dtype=dtype, coarse=coarse, transport="p2p")
         fs = f[c0:c1].contiguous()
         out = plan.solve(fs)
         torch.cuda.synchronize()
@@ -60,15 +63,21 @@ def _rank_main(rank, world, port, case, q):
 def test_p2p_sharded_processes_match_unsharded(fm, case):
     import torch
 
-    m, P, b, n_sr, B, S, coarse = case
+    m, P, b, n_sr, B, S, coarse, dt = case
+    dtype = torch.float64 if dt == "f64" else torch.float32
     want = fm.fmg_solve(_cfg(fm, m, P, b, n_sr),
-                        fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + S))[0],
+                        fm.fourier_batch(2 ** m, fm.fourier_coefficients(B, seed=m + S),
+                                         dtype)[0],
                         coarse=coarse)[0]
     torch.cuda.synchronize()
     want = want.cpu().numpy()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29900 + (os.getpid() % 400) + S
+    import socket
+
+    with socket.socket() as sk:  # a free port for this group's rendezvous
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     procs = [ctx.Process(target=_rank_main, args=(r, S, port, case, q)) for r in range(S)]
     for p in procs:
         p.start()
