@@ -59,7 +59,7 @@ __host__ __device__ inline double pow4(int k) {
   return __longlong_as_double_hd((long long)(1023 + 2 * k) << 52);
 }
 // launch shapes of the visit kernel (visit_impl.cuh VisitShape)
-enum { SHAPE_WIDE = 0, SHAPE_DEEP = 1 };
+enum { SHAPE_WIDE = 0, SHAPE_DEEP = 1, SHAPE_R4 = 2 };
 // SM sub-partitions (4 per SM) of the current device (kernels_visit.cu)
 int visit_smsps();
 inline bool is_pow2(i64 n) { return n >= 1 && (n & (n - 1)) == 0; }

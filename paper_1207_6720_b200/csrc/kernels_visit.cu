@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "fmgsr_chain.cuh"
 #include "fmgsr_internal.h"
@@ -99,6 +100,36 @@ static bool visit_cpl2_ok(const VisitDesc<T>& d) {
          al(d.fun_part);
 }
 
+// R4 launch shape (4-pair ring, 128-register bound: four CTAs per SM) for the
+// two-column fp64 down visits (plain load + fused restriction: 160 registers
+// and a 64 KB ring hold WIDE to three CTAs per SM) and FAS-correction up
+// visits (an 80 KB ring holds WIDE to two), when the launch has more warps
+// than one WIDE wave (148 SMs x 12 warps): then the fuller last wave and the
+// extra resident warps outweigh the shallower ring.  Measured on config 4
+// (4096 warps per visit, tools/visit_breakdown.py): level-17..23 down visits
+// 3-7 % and up visits 1-7 % faster; with fewer warps than one wave (config 2,
+// 1024) the shallower ring loses (3.029 -> 3.050 ms), and the FMG top visits
+// spill at 128 registers, so they stay WIDE.  FMGSR_VISIT_R4 = 0 (never),
+// d / du (down / down and up visits regardless of size), all (every
+// two-column fp64 visit) for A/B runs.
+template <typename T>
+static bool visit_r4(const VisitDesc<T>& d) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FMGSR_VISIT_R4");
+    const std::string x = e ? e : "";
+    v = x == "0" ? 0 : x == "d" ? 1 : x == "du" ? 2 : x == "all" ? 3 : 4;
+  }
+  const bool down = d.src == SRC_LOAD && d.epi, up = d.src == SRC_CORR && !d.epi && !d.cr;
+  if (v == 0) return false;
+  if (v == 3) return true;
+  if (v == 1) return down;
+  if (v == 2) return down || up;
+  const i64 P = d.p_count >= 0 ? d.p_count : d.n / d.W;
+  const i64 warps = P * ((d.B / 2 + 31) / 32);
+  return (down || up) && warps > 12 * (i64)visit_smsps() / 4;
+}
+
 template <typename T>
 void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   require(d.n >= 2 && is_pow2(d.n), "visit: level size must be a power of two >= 2");
@@ -131,7 +162,12 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
     require(!d.fun_part, "visit: no functional output with fp64 arithmetic on fp32 fields");
     visit_launch_mixed(d, visit_cpl2_ok(d), visit_few_chains(d), s);
   } else if (visit_cpl2_ok(d)) {
-    visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
+    bool r4 = false;
+    if constexpr (std::is_same<T, double>::value) {
+      r4 = visit_r4(d);
+      if (r4) visit_fill_launch<V2<T>, T, SHAPE_R4>(d, s);
+    }
+    if (!r4) visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
   } else if (visit_few_chains(d)) {
     visit_fill_launch<T, T, SHAPE_DEEP>(d, s);
   } else {

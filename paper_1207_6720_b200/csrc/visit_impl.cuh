@@ -40,10 +40,13 @@ struct VisitArgs {
 // 16-pair ring -- few chains (at most one warp per SM sub-partition, scalar
 // lanes: config-5 P = 16 / 64): a warp issues alone, so its own ring must
 // cover the DRAM latency while the fast loop fetches two pairs ahead.
+// R4: 4-pair ring and a 128-register bound -- four CTAs per SM for the visits
+// whose 8-pair ring and register count hold them to two or three (A/B:
+// FMGSR_VISIT_R4)
 template <int SHAPE>
 struct VisitShape {
   static constexpr int NT = 128;
-  static constexpr int D = SHAPE == SHAPE_WIDE ? 8 : 16;
+  static constexpr int D = SHAPE == SHAPE_WIDE ? 8 : SHAPE == SHAPE_DEEP ? 16 : 4;
 };
 
 template <typename M, int SRC, bool CR, int NT, int D>
@@ -57,7 +60,7 @@ __host__ __device__ constexpr size_t visit_smem_bytes() {  // staging ring + one
 
 template <typename T, int SRC, bool CR, bool EPI, bool OMEGA1, bool BULK, bool FUNC, int NT, int D,
           typename M = T>
-__global__ void __launch_bounds__(NT, (sizeof(T) > 8 ? 256 : 512) / NT)
+__global__ void __launch_bounds__(NT, (D <= 4 ? 512 : (sizeof(T) > 8 ? 256 : 512)) / NT)
     visit_kernel(const VisitArgs<T, M> a) {
   extern __shared__ __align__(128) unsigned char visit_smem[];
   const int lane = threadIdx.x & 31;
