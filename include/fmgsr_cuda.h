@@ -332,6 +332,13 @@ int fmgsr_shard_plan_create_p2p(const fmgsr_plan_desc* desc, int32_t shards, int
 int fmgsr_shard_p2p_export(void* plan, void* buf, int64_t cap, int64_t* len);
 int fmgsr_shard_p2p_import(void* plan, const void* all, int64_t per_rank);
 int fmgsr_shard_p2p_status(void* plan, int32_t* err);
+/* A sharded plan's own finest-level forcing buffer: *slab = the DEVICE address
+ * of this rank's [rows][ld] slab inside it (the plan keeps halo rows around
+ * it), *rows = 2^m / shards.  A caller that writes its forcing there and passes
+ * that address as `forcing` to fmgsr_plan_solve saves the slab copy into the
+ * plan (2 x the slab bytes of HBM traffic per solve); any other forcing
+ * address is copied as before.  Valid until fmgsr_plan_destroy. */
+int fmgsr_shard_plan_forcing_slab(void* plan, void** slab, int64_t* rows);
 /* Virtual shards: all S shards of one problem on the current device, run in
  * lockstep on one stream (transfers are device copies).  forcing / solution
  * are the full DEVICE [2^m][ld] arrays; the result is bit-identical to the

@@ -114,6 +114,7 @@ _SIGS = {
     "fmgsr_shard_group_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fmgsr_shard_group_cutoff": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i64)]),
     "fmgsr_shard_group_destroy": (C.c_int, [_vp]),
+    "fmgsr_shard_plan_forcing_slab": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_i64)]),
     "fmgsr_shard_plan_create_local": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, C.POINTER(_vp)]),
     "fmgsr_shard_plan_create_p2p": (C.c_int, [C.POINTER(PlanDesc), _i32, _i32, C.POINTER(_vp)]),
     "fmgsr_shard_p2p_export": (C.c_int, [_vp, _vp, _i64, C.POINTER(_i64)]),

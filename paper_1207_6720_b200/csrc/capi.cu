@@ -128,6 +128,11 @@ struct PlanBase {
     throw Error(ERR_ARG, "not a peer-memory shard plan");
   }
   virtual int p2p_status() { throw Error(ERR_ARG, "not a peer-memory shard plan"); }
+  // a sharded plan's own finest forcing buffer (slab rows, halo rows around them)
+  virtual void* forcing_slab(i64* rows) {
+    (void)rows;
+    throw Error(ERR_ARG, "not a sharded plan");
+  }
 };
 
 template <typename T>
@@ -192,6 +197,17 @@ struct Plan : PlanBase {
   int S = 1, srank = 0, Lr = 1 << 30;
   i64 H = 0;
   T* fm = nullptr;  // sharded finest forcing (slab + halo)
+  T* fm_base = nullptr;  // its allocation
+  // the caller may fill the plan's own forcing slab (forcing_slab()) and pass
+  // it to solve: then ST_LOADF has nothing to copy
+  bool forcing_in_place(const T* forcing) const {
+    return S > 1 && forcing == fm + c0(d.m) * d.ld;
+  }
+  void* forcing_slab(i64* rows) override {
+    require(S > 1 && fm, "forcing_slab: not a sharded plan");
+    if (rows) *rows = c1(d.m) - c0(d.m);
+    return fm + c0(d.m) * d.ld;
+  }
   std::vector<T*> ob, ib;  // per-level edge-record outbox / inbox (2 slots x 5 x Bp)
   bool sharded(int l) const { return S > 1 && l > Lr; }
   i64 c0(int l) const { return (lv[l].n / S) * srank; }
@@ -437,7 +453,7 @@ struct Plan : PlanBase {
         L.ub[1] = L.u[1] - shift;
         L.ubytes = fb;
         if (l < m) L.f = alloc(fb) + shift;
-        else fm = alloc(fb) + shift;
+        else fm = (fm_base = alloc(fb)) + shift;
         ob[l] = alloc((size_t)10 * Bp * sizeof(T));
         ib[l] = alloc((size_t)10 * Bp * sizeof(T));
       } else {
@@ -961,7 +977,7 @@ struct Plan : PlanBase {
   void enqueue(const T* forcing, T* solution, cudaStream_t s) {
     const int m0 = d.m0, m = d.m;
     reset_state(s);
-    poison_all(s);
+    poison_all(s, forcing_in_place(forcing) ? fm_base : nullptr);
     if (use_coarse) {
       enqueue_coarse(forcing, solution, s);
       return;
@@ -1064,7 +1080,7 @@ struct Plan : PlanBase {
   void run_step(const Step& st, const T* forcing, T* solution, cudaStream_t s) {
     switch (st.kind) {
       case ST_LOADF:  // the caller's forcing slab into the halo'd finest buffer
-        if (!dry)
+        if (!dry && !forcing_in_place(forcing))
           check_cuda(cudaMemcpyAsync(fm + c0(d.m) * d.ld, forcing,
                                    (size_t)(c1(d.m) - c0(d.m)) * d.ld * sizeof(T),
                                    cudaMemcpyDeviceToDevice, s),
@@ -1497,10 +1513,10 @@ struct Plan : PlanBase {
     }
   }
 
-  void poison_all(cudaStream_t s) {
+  void poison_all(cudaStream_t s, const void* keep = nullptr) {
     if (dry || !(debug & FMGSR_DEBUG_POISON)) return;
     for (size_t k = 0; k < n_field_allocs; k++)
-      check_cuda(cudaMemsetAsync(alloc_user[k], 0xFF, alloc_sizes[k], s), "poison");
+      if (alloc_user[k] != keep) check_cuda(cudaMemsetAsync(alloc_user[k], 0xFF, alloc_sizes[k], s), "poison");
   }
   // after FMG step t: the SR levels below t are dead (levels <= Lc live on chip)
   void poison_sr_below(int t, cudaStream_t s) {
@@ -2334,6 +2350,14 @@ int fmgsr_shard_p2p_status(void* plan, int32_t* err) {
   return guarded([&] {
     require(plan && err, "shard_p2p_status: null argument");
     *err = static_cast<PlanBase*>(plan)->p2p_status();
+  });
+}
+int fmgsr_shard_plan_forcing_slab(void* plan, void** slab, int64_t* rows) {
+  return guarded([&] {
+    require(plan && slab, "shard_plan_forcing_slab: null argument");
+    i64 r = 0;
+    *slab = static_cast<PlanBase*>(plan)->forcing_slab(&r);
+    if (rows) *rows = r;
   });
 }
 int fmgsr_shard_plan_create_local(const fmgsr_plan_desc* desc, int32_t shards, int32_t rank,

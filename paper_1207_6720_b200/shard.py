@@ -86,6 +86,18 @@ class ShardGroup:
         return out
 
 
+class _DeviceView:
+    """A device array owned by a plan, exposed through __cuda_array_interface__
+    (the tensor made from it keeps this object, and so the plan, alive)."""
+
+    def __init__(self, ptr: int, shape, dtype, owner):
+        self._owner = owner
+        typestr = {torch.float64: "<f8", torch.float32: "<f4"}[dtype]
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2,
+                                         "strides": None}
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     N.check(N.lib().fmgsr_nccl_unique_id(buf), "nccl_unique_id")
@@ -149,6 +161,18 @@ class ShardedPlan:
                 raise ValueError("p2p exchange: expected one blob per rank of equal size")
             allb = (C.c_uint8 * (n.value * shards)).from_buffer_copy(b"".join(blobs))
             N.check(N.lib().fmgsr_shard_p2p_import(h, allb, n.value), "shard_p2p_import")
+
+    def forcing_slab(self) -> torch.Tensor:
+        """The plan's own finest-level forcing slab as a (rows, B) CUDA tensor
+        (fmgsr_shard_plan_forcing_slab).  Fill it and pass it to ``solve``: the
+        solve then reads the forcing where it lies instead of first copying the
+        caller's slab into the plan (2 x the slab bytes of HBM traffic)."""
+        ptr, rows = C.c_void_p(), C.c_int64()
+        N.check(N.lib().fmgsr_shard_plan_forcing_slab(self._h, C.byref(ptr), C.byref(rows)),
+                "shard_plan_forcing_slab")
+        k = self.key
+        return torch.as_tensor(_DeviceView(ptr.value, (rows.value, k.B), k.dtype, self),
+                               device="cuda")
 
     def status(self) -> int:
         """p2p transport: synchronise and return 0, or non-zero if a peer wait timed out."""

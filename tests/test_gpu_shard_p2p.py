@@ -51,12 +51,19 @@ def _rank_main(rank, world, port, case, q):
         torch.cuda.synchronize()
         first = out.cpu().numpy().copy()
         out2 = plan.solve(fs)  # graph replay: the epoch advances on the device
+        second = out2.cpu().numpy().copy()
+        # the forcing written into the plan's own slab: solved in place (no slab copy)
+        own = plan.forcing_slab()
+        assert tuple(own.shape) == tuple(fs.shape) and own.dtype == fs.dtype
+        own.copy_(fs)
+        out3 = plan.solve(own)
+        out3 = plan.solve(own)  # and its graph replayed
         err = plan.status()
-        q.put((rank, first, out2.cpu().numpy(), err, None))
+        q.put((rank, first, second, out3.cpu().numpy(), err, None))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # reported to the parent, never a hang
-        q.put((rank, None, None, -1, f"{type(e).__name__}: {e}"))
+        q.put((rank, None, None, None, -1, f"{type(e).__name__}: {e}"))
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -84,17 +91,18 @@ def test_p2p_sharded_processes_match_unsharded(fm, case):
     res = {}
     try:
         for _ in procs:
-            r, a, a2, err, msg = q.get(timeout=240)
-            res[r] = (a, a2, err, msg)
+            r, a, a2, a3, err, msg = q.get(timeout=240)
+            res[r] = (a, a2, a3, err, msg)
     finally:
         for p in procs:
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
     for r in range(S):
-        a, a2, err, msg = res[r]
+        a, a2, a3, err, msg = res[r]
         assert msg is None, f"rank {r}: {msg}"
         assert err == 0, f"rank {r}: a peer wait timed out"
         rows = 2 ** m // S
         assert np.array_equal(a, want[r * rows:(r + 1) * rows]), f"rank {r} differs"
         assert np.array_equal(a2, a), f"rank {r}: graph replay differs"
+        assert np.array_equal(a3, a), f"rank {r}: in-place forcing slab differs"
