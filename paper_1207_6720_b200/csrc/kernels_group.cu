@@ -1,4 +1,4 @@
-// kernels_group.cu -- level visits of SHORT patches (owned width W <= 16).
+// kernels_group.cu -- level visits of SHORT patches (owned width W <= 8).
 //
 // On the mid levels of a deep hierarchy (config 4: levels 13-16, 4096 patches
 // of 2-16 cells with an 8-cell buffer) a patch chain is 10-24 cells long, so
@@ -49,6 +49,8 @@ struct GroupArgs {
   int* cnt;
 };
 
+constexpr int GROUP_NT = 128;  // threads per group CTA (4 warps)
+
 template <typename T, bool OMEGA1>
 __device__ __forceinline__ T gs_interior(const GsCoef<T>& gc, T l, T u, T r, T f) {
   T s = xsub(xsub(xmul(T(2), u), l), r);
@@ -57,11 +59,13 @@ __device__ __forceinline__ T gs_interior(const GsCoef<T>& gc, T l, T u, T r, T f
   return xadd(u, xmul(resid, gc.rdiag));
 }
 
-// One warp per (group, 32 RHS columns); one lane per column.
+// One CTA of NW warps per (group, 32 RHS columns); one lane per column, the
+// group's rows, chains and coarse cells dealt round-robin to the warps.
 template <typename T, int SRC, bool EPI, bool OMEGA1, int IL>
-__global__ void __launch_bounds__(32) group_visit_kernel(const GroupArgs<T> a) {
+__global__ void __launch_bounds__(GROUP_NT) group_visit_kernel(const GroupArgs<T> a) {
   extern __shared__ __align__(16) unsigned char group_smem[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = GROUP_NT / 32;
   const unsigned nrg = (unsigned)a.nrg;
   const unsigned g = nrg == 1 ? blockIdx.x : blockIdx.x / nrg;
   const int rg = (int)(blockIdx.x - g * nrg);
@@ -79,41 +83,52 @@ __global__ void __launch_bounds__(32) group_visit_kernel(const GroupArgs<T> a) {
   const i64 ulo = wlo > 0 ? wlo - 1 : 0;      // smoother input rows [ulo, uhi)
   const i64 uhi = oe < n ? oe + 1 : n;
 
-  T* Us = reinterpret_cast<T*>(group_smem) + lane;  // row k of this lane: Us[k * 32]
+  T* Us = reinterpret_cast<T*>(group_smem) + lane;  // row k of this column: Us[k * 32]
   T* Fs = Us + a.rows_u * 32;
   T* Hs = Fs + a.rows_f * 32;
   T* Ns = Hs + a.rows_h * 32;  // smoothed owned cells (EPI)
-  const T* f = a.f + rr;
   i64 ubase;  // the cell held by row 0 of Us
 
-  for (i64 i = wlo; i < oe; i++) cp_async(Fs + (int)(i - wlo) * 32, f + i * ld);
+  {
+    const int nf = (int)(oe - wlo);
+    const T* src = a.f + rr + (wlo + w) * ld;
+    T* dst = Fs + w * 32;
+    for (int k = w; k < nf; k += NW, src += NW * ld, dst += NW * 32) cp_async(dst, src);
+  }
   if (SRC == SRC_LOAD) {
-    const T* u = a.u_src + rr;
     ubase = ulo;
-    for (i64 i = ulo; i < uhi; i++) cp_async(Us + (int)(i - ulo) * 32, u + i * ld);
+    const int nu = (int)(uhi - ulo);
+    const T* src = a.u_src + rr + (ulo + w) * ld;
+    T* dst = Us + w * 32;
+    for (int k = w; k < nu; k += NW, src += NW * ld, dst += NW * 32) cp_async(dst, src);
     cp_commit();
     cp_wait<0>();
+    __syncthreads();
   } else {
     // u + P(uH - R u) on the pairs [q0, q1] needs c = uH - R u one pair further out
-    const T* u = a.u_src + rr;
-    const T* uH = a.uH + rr;
     const i64 nc = a.nc;
     const i64 q0 = ulo >> 1, q1 = (uhi - 1) >> 1;
     const i64 rq0 = q0 > 0 ? q0 - 1 : 0, rq1 = q1 < nc - 1 ? q1 + 1 : nc - 1;
     ubase = 2 * rq0;
-    for (i64 j = rq0; j <= rq1; j++) {
-      const int k = (int)(j - rq0);
-      cp_async(Us + (2 * k) * 32, u + (2 * j) * ld);
-      cp_async(Us + (2 * k + 1) * 32, u + (2 * j + 1) * ld);
-      cp_async(Hs + k * 32, uH + j * ld);
+    const int np = (int)(rq1 - rq0 + 1);
+    {
+      const T* su = a.u_src + rr + (2 * (rq0 + w)) * ld;
+      const T* sh = a.uH + rr + (rq0 + w) * ld;
+      for (int k = w; k < np; k += NW, su += 2 * NW * ld, sh += NW * ld) {
+        cp_async(Us + (2 * k) * 32, su);
+        cp_async(Us + (2 * k + 1) * 32, su + ld);
+        cp_async(Hs + k * 32, sh);
+      }
     }
     cp_commit();
     cp_wait<0>();
-    const int np = (int)(rq1 - rq0 + 1);
-    for (int k = 0; k < np; k++)  // c_j = uH[j] - 0.5 (u[2j] + u[2j+1])
+    __syncthreads();
+    for (int k = w; k < np; k += NW)  // c_j = uH[j] - 0.5 (u[2j] + u[2j+1])
       Hs[k * 32] = xsub(Hs[k * 32], xmul(T(0.5), xadd(Us[(2 * k) * 32], Us[(2 * k + 1) * 32])));
-    for (i64 q = q0; q <= q1; q++) {  // PairSource<SRC_CORR>::make, pair q
-      const int k = (int)(q - rq0);
+    __syncthreads();
+    const int k0 = (int)(q0 - rq0), k1 = (int)(q1 - rq0);
+    for (int k = k0 + w; k <= k1; k += NW) {  // PairSource<SRC_CORR>::make, pair rq0 + k
+      const i64 q = rq0 + k;
       const T s1 = Hs[k * 32], s2 = Us[(2 * k) * 32], s3 = Us[(2 * k + 1) * 32];
       const T p0v = (q == 0) ? xmul(T(0.5), s1)
                              : xmul(T(0.25), xadd(Hs[(k - 1) * 32], xmul(T(3), s1)));
@@ -122,44 +137,54 @@ __global__ void __launch_bounds__(32) group_visit_kernel(const GroupArgs<T> a) {
       Us[(2 * k) * 32] = xadd(s2, p0v);
       Us[(2 * k + 1) * 32] = xadd(s3, p1v);
     }
+    __syncthreads();
   }
 
-  // ---- the group's patch chains, IL at a time ------------------------------------
+  // ---- the group's patch chains: IL per warp at a time ---------------------------
   const GsCoef<T> gc = a.gc;
   T* out = ((!EPI || a.write_u) && a.u_out) ? a.u_out + rr : nullptr;
   const int uo = (int)(os - ubase), fo = (int)(os - wlo);  // row of cell `os` in Us / Fs
   // interior groups: every smoothed cell has both neighbours and all IL-blocks are full
   const bool bnd = (os - b - 1 < 0) || (oe >= n) || (Gp % IL != 0);
   if (!bnd) {
-    for (int k0 = 0; k0 < Gp; k0 += IL) {
+    for (int k0 = w * IL; k0 < Gp; k0 += NW * IL) {
       T uL[IL];
       const T* up = Us + (uo + k0 * W - b) * 32;  // chain c: cell os + (k0 + c) W - b + t
       const T* fp = Fs + (fo + k0 * W - b) * 32;
+      T cu[IL];  // the current cell's input: the right neighbour read one step earlier
 #pragma unroll
-      for (int c = 0; c < IL; c++) uL[c] = up[(c * W - 1) * 32];
+      for (int c = 0; c < IL; c++) {
+        uL[c] = up[(c * W - 1) * 32];
+        cu[c] = up[(c * W) * 32];
+      }
       for (int t = 0; t < b; t++) {  // buffer cells left of each patch
 #pragma unroll
         for (int c = 0; c < IL; c++) {
           const int x = (c * W + t) * 32;
-          uL[c] = gs_interior<T, OMEGA1>(gc, uL[c], up[x], up[x + 32], fp[x]);
+          const T nx = up[x + 32];
+          uL[c] = gs_interior<T, OMEGA1>(gc, uL[c], cu[c], nx, fp[x]);
+          cu[c] = nx;
         }
       }
-      for (int t = b; t < b + W; t++) {  // owned cells
+      T* po = out ? out + (os + (i64)k0 * W) * ld : nullptr;
+      T* pn = Ns + (k0 * W) * 32;
+      for (int t = 0; t < W; t++) {  // owned cells
 #pragma unroll
         for (int c = 0; c < IL; c++) {
-          const int x = (c * W + t) * 32;
-          const T v = gs_interior<T, OMEGA1>(gc, uL[c], up[x], up[x + 32], fp[x]);
+          const int x = (c * W + b + t) * 32;
+          const T nx = up[x + 32];
+          const T v = gs_interior<T, OMEGA1>(gc, uL[c], cu[c], nx, fp[x]);
           uL[c] = v;
-          const int oc = (k0 + c) * W + t - b;  // owned cell index within the group
-          if (EPI) Ns[oc * 32] = v;
-          if (out) out[(os + oc) * ld] = v;
+          cu[c] = nx;
+          if (EPI) pn[(c * W + t) * 32] = v;
+          if (po) po[(i64)(c * W + t) * ld] = v;
         }
       }
     }
   } else {
     // groups at a domain end or partly filled: the same chains, every cell
     // through the general gs_cell (domain rows first, as the reference)
-    for (int k = 0; k < Gp; k++) {
+    for (int k = w; k < Gp; k += NW) {
       const i64 pos = os + (i64)k * W;
       const i64 ws = pos - b > 0 ? pos - b : 0;
       T uL = ws > 0 ? Us[(int)(ws - 1 - ubase) * 32] : T(0);
@@ -176,52 +201,98 @@ __global__ void __launch_bounds__(32) group_visit_kernel(const GroupArgs<T> a) {
     }
   }
   if (!EPI) return;
+  __syncthreads();
 
-  // ---- restriction + tau over the group's owned pairs ----------------------------
-  Epilogue<T, T> ep;
-  ep.inv_h2 = gc.inv_h2;
-  ep.inv_H2 = a.inv_H2;
-  ep.left_dom = (os == 0);
-  ep.right_dom = (oe == n);
-  ep.write_uH = a.uH_out != nullptr;
-  ep.uH_out = a.uH_out ? a.uH_out + rr : nullptr;
-  ep.fH_out = a.fH_out + rr;
-  ep.ld = ld;
-  ep.nc = a.nc;
-  ep.cnt = 0;
-  ep.up2 = ep.up1 = ep.Lprev = ep.Rm2 = ep.Rm1 = ep.Rfm1 = T(0);
+  // ---- restriction + tau over the group's owned cells (stencils.py:108-125) ------
+  // One coarse cell per (warp, step), each from the smoothed cells in Ns with
+  // the expressions of Epilogue::push / finish; the first and last coarse cell
+  // of the group need the neighbour group's cells: edge records, as visit_kernel.
+  const T ih = gc.inv_h2, iH = a.inv_H2;
+  const bool left_dom = (os == 0), right_dom = (oe == n);
   const i64 j0 = os >> 1;
-  const int npair = (int)((oe - os) >> 1);  // >= 2 (G W >= 4)
+  const int ncg = (int)((oe - os) >> 1);  // coarse cells of the group, >= 2
   const T* Fo = Fs + fo * 32;
-  ep.push(j0, Ns[0], Ns[32], Fo[0], Fo[32], true);
-  ep.push(j0 + 1, Ns[2 * 32], Ns[3 * 32], Fo[2 * 32], Fo[3 * 32], true);
-  ep.fast_begin(j0 + 2);
-  if (ep.write_uH) {
-    for (int k = 2; k < npair; k++)
-      ep.template push_fast<true>(Ns[(2 * k) * 32], Ns[(2 * k + 1) * 32], Fo[(2 * k) * 32],
-                                  Fo[(2 * k + 1) * 32]);
-  } else {
-    for (int k = 2; k < npair; k++)
-      ep.template push_fast<false>(Ns[(2 * k) * 32], Ns[(2 * k + 1) * 32], Fo[(2 * k) * 32],
-                                   Fo[(2 * k + 1) * 32]);
-  }
-  EdgeRec<T> right;
-  ep.finish(true, right);
-  const i64 ldE = (i64)a.nrg * 32;
-  // slab edges of a shard go to the outbox (the neighbour shard finishes them)
-  const bool remL = !ep.left_dom && g == 0 && a.left_remote;
-  const bool remR = !ep.right_dom && (i64)g == a.ngroups - 1 && a.right_remote;
-  if (remL) {
+  T* fH = a.fH_out + rr;
+  T* uHo = a.uH_out ? a.uH_out + rr : nullptr;
+  auto N = [&](int i) { return Ns[i * 32]; };                 // smoothed owned cell os + i
+  auto Ru = [&](int c) { return xmul(T(0.5), xadd(N(2 * c), N(2 * c + 1))); };
+  auto Lu = [&](int i) { return xmul(xsub(xsub(xmul(T(2), N(i)), N(i - 1)), N(i + 1)), ih); };
+  if (w == 0) {
+    // slab edges of a shard go to the outbox (the neighbour shard finishes them)
+    EdgeRec<T> left, right;
+    if (!left_dom) {
+      left.v[0] = N(0);
+      left.v[1] = N(1);
+      left.v[2] = Lu(1);
+      left.v[3] = Ru(1);
+      left.v[4] = xmul(T(0.5), xadd(Fo[0], Fo[32]));
+    }
+    if (!right_dom) {
+      const int s = 2 * ncg;
+      right.v[0] = N(s - 2);
+      right.v[1] = N(s - 1);
+      right.v[2] = Lu(s - 2);
+      right.v[3] = Ru(ncg - 2);
+      right.v[4] = xmul(T(0.5), xadd(Fo[(s - 2) * 32], Fo[(s - 1) * 32]));
+    }
+    const i64 ldE = (i64)a.nrg * 32;
+    const bool remL = !left_dom && g == 0 && a.left_remote;
+    const bool remR = !right_dom && (i64)g == a.ngroups - 1 && a.right_remote;
+    if (remL) {
 #pragma unroll
-    for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = ep.left.v[k];
-  }
-  if (remR) {
+      for (int k = 0; k < 5; k++) a.E_out[(0 * 5 + k) * ldE + r] = left.v[k];
+    }
+    if (remR) {
 #pragma unroll
-    for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
+      for (int k = 0; k < 5; k++) a.E_out[(1 * 5 + k) * ldE + r] = right.v[k];
+    }
+    edge_arrive2<T, false, T>(a.E, a.cnt, ldE, a.nrg, lane, rg, r, true, fH, ld, ih, iH,
+                              !left_dom && !remL, p0, left, os, !right_dom && !remR, p0 + Gp,
+                              right, oe);
   }
-  edge_arrive2<T, false, T>(a.E, a.cnt, ldE, a.nrg, lane, rg, r, true, ep.fH_out, ld, ep.inv_h2,
-                            ep.inv_H2, !ep.left_dom && !remL, p0, ep.left, os,
-                            !ep.right_dom && !remR, p0 + Gp, right, oe);
+  // a contiguous run of coarse cells per warp, sliding over the smoothed cells
+  // (each read once); warp 0 (busy with the edge protocol) takes the last,
+  // possibly short, run
+  const int per = (ncg + NW - 1) / NW;
+  const int cb = (NW - 1 - w) * per, ce = cb + per < ncg ? cb + per : ncg;
+  if (cb >= ce) return;
+  T nm1 = cb > 0 ? N(2 * cb - 1) : T(0), Rm = cb > 0 ? Ru(cb - 1) : T(0);
+  T n0 = N(2 * cb), n1 = N(2 * cb + 1);
+  T Rc = xmul(T(0.5), xadd(n0, n1));
+  for (int c = cb; c < ce; c++) {
+    T n2 = T(0), n3 = T(0), Rn = T(0);
+    if (c + 1 < ncg) {
+      n2 = N(2 * c + 2);
+      n3 = N(2 * c + 3);
+      Rn = xmul(T(0.5), xadd(n2, n3));
+    }
+    if (uHo) uHo[(j0 + c) * ld] = Rc;
+    const T Le = xmul(xsub(xsub(xmul(T(2), n0), nm1), n1), ih);  // Lu at the pair's even cell
+    const T Lo = xmul(xsub(xsub(xmul(T(2), n1), n0), n2), ih);   // ... and its odd cell
+    T LH, RL;
+    bool emit = true;
+    if (c == 0) {
+      emit = left_dom;  // otherwise completed through the edge records
+      LH = xmul(xsub(xmul(T(3), Rc), Rn), iH);
+      RL = xmul(T(0.5), xadd(xmul(xsub(xmul(T(3), n0), n1), ih), Lo));
+    } else if (c == ncg - 1) {
+      emit = right_dom;
+      LH = xmul(xsub(xmul(T(3), Rc), Rm), iH);
+      RL = xmul(T(0.5), xadd(Le, xmul(xsub(xmul(T(3), n1), n0), ih)));
+    } else {
+      LH = xmul(xsub(xsub(xmul(T(2), Rc), Rm), Rn), iH);
+      RL = xmul(T(0.5), xadd(Le, Lo));
+    }
+    if (emit) {
+      const T Rf = xmul(T(0.5), xadd(Fo[(2 * c) * 32], Fo[(2 * c + 1) * 32]));
+      fH[(j0 + c) * ld] = xadd(Rf, xsub(LH, RL));
+    }
+    nm1 = n1;
+    Rm = Rc;
+    n0 = n2;
+    n1 = n3;
+    Rc = Rn;
+  }
 }
 
 template <typename T, int SRC, bool EPI, bool OMEGA1, int IL>
@@ -229,13 +300,14 @@ void launch_group_k(const GroupArgs<T>& a, size_t smem, cudaStream_t s) {
   auto k = group_visit_kernel<T, SRC, EPI, OMEGA1, IL>;
   if (smem > 48 * 1024)
     require(smem <= (size_t)smem_optin((const void*)k), "group visit: shared memory budget exceeded");
-  k<<<(unsigned)(a.ngroups * a.nrg), 32, smem, s>>>(a);
+  k<<<(unsigned)(a.ngroups * a.nrg), GROUP_NT, smem, s>>>(a);
 }
 
 template <typename T, int SRC, bool EPI>
 void launch_group_il(const GroupArgs<T>& a, size_t smem, cudaStream_t s) {
   const bool om1 = a.gc.omega == T(1);
-  const int il = a.G >= 4 ? 4 : a.G;
+  const int per_warp = a.G / (GROUP_NT / 32);  // chains per warp (G is a power of two)
+  const int il = per_warp >= 4 ? 4 : per_warp >= 2 ? 2 : 1;
 #define FMGSR_GROUP_IL(ILV)                                              \
   if (om1) launch_group_k<T, SRC, EPI, true, ILV>(a, smem, s);           \
   else launch_group_k<T, SRC, EPI, false, ILV>(a, smem, s);
@@ -259,6 +331,17 @@ bool group_enabled() {
   return v == 1;
 }
 
+// widest owned width served here (FMGSR_GROUP_MAXW overrides, for A/B runs)
+int group_max_w() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FMGSR_GROUP_MAXW");
+    v = e ? atoi(e) : 8;
+    if (v > 16) v = 16;
+  }
+  return v;
+}
+
 }  // namespace
 
 // Short-patch visits (plain-load down visits with or without the fused
@@ -269,7 +352,10 @@ template <typename T>
 bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s) {
   if (!group_enabled() || d.olo || d.cr || d.fun_part || d.f64_arith) return false;
   if (!(d.src == SRC_LOAD || (d.src == SRC_CORR && !d.epi))) return false;
-  if (d.W < 2 || d.W > 16 || (d.W & (d.W - 1)) != 0 || d.b < 0 || d.b > 32 || d.n < 8) return false;
+  // W = 16 measured slower than the streaming kernel (config 4 level 16: 49 / 42 us
+  // against 40 / 33 us per down / up visit): two chains per group leave two of
+  // the four warps without chain work
+  if (d.W < 2 || d.W > group_max_w() || (d.W & (d.W - 1)) != 0 || d.b < 0 || d.b > 32 || d.n < 8) return false;
   const i64 Plev = d.n / d.W;
   const i64 P = d.p_count >= 0 ? d.p_count : Plev;
   if (P == 0) return true;  // nothing to do

@@ -59,6 +59,10 @@ static bool visit_few_chains(const VisitDesc<T>& d) {
   return warps1 <= visit_smsps();
 }
 
+// short patches (W <= 16): one warp per group of patches (kernels_group.cu)
+template <typename T>
+bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s);
+
 // the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
 // compiled in parallel)
 template <typename TV, typename T, int SHAPE, typename TM = TV>
@@ -158,6 +162,7 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
+  if (try_group_visit(d, s)) return;
   if (d.f64_arith) {
     require(!d.fun_part, "visit: no functional output with fp64 arithmetic on fp32 fields");
     visit_launch_mixed(d, visit_cpl2_ok(d), visit_few_chains(d), s);
