@@ -215,6 +215,15 @@ struct Plan : PlanBase {
 
   bool is_sr(int l) const { return l > d.m - d.n_sr; }
 
+  // Levels whose visits carry the fused restriction + tau epilogue (edge
+  // records and counters allocated): owned width >= 4, or width 2 where the
+  // short-patch group kernel serves the down visits (a group owns >= 4 cells).
+  bool group_w2(const Level& L) const {
+    return d.fused && d.ns == 1 && !d.nonlinear && !mixed && L.W == 2 && L.n >= 8 &&
+           group_visit_enabled();
+  }
+  bool epi_level(const Level& L) const { return L.W >= 4 || group_w2(L); }
+
   // Dry plans (fmgsr_shard_schedule) run the host logic only -- geometry,
   // cutoffs, the step list and its level ping-pong state -- with every device
   // call skipped and fake addresses, so the communication schedule can be
@@ -332,7 +341,7 @@ struct Plan : PlanBase {
         if (rows > scratch_rows) scratch_rows = rows;
       }
       if (l > m0) tmp_rows = L.n > tmp_rows ? L.n : tmp_rows;
-      if (l > m0 && L.W >= 4) cnt_total += (L.n / L.W + 1) * nrg;
+      if (l > m0 && epi_level(L)) cnt_total += (L.n / L.W + 1) * nrg;
     }
     // Coarse cutoff: about 128 CTAs of CW columns; the deepest level whose
     // three fields per level (two u, f) for CW columns fit in ~200 KB.
@@ -465,7 +474,7 @@ struct Plan : PlanBase {
         L.ubytes = fb;
         if (l < m) L.f = alloc(fb);
       }
-      if (l > m0 && L.W >= 4) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * esz());
+      if (l > m0 && epi_level(L)) L.E = alloc((size_t)(L.n / L.W + 1) * 10 * Bp * esz());
     }
     tmp = alloc((size_t)tmp_rows * ld * sizeof(T));
     if (!dry)
@@ -485,7 +494,7 @@ struct Plan : PlanBase {
     i64 off = 0;
     for (int l = m0 + 1; l <= m; l++) {
       Level& L = lv[l];
-      if (L.W >= 4) {
+      if (epi_level(L)) {
         L.cnt = cnt_all + off;
         off += (L.n / L.W + 1) * nrg;
       }
@@ -829,7 +838,9 @@ struct Plan : PlanBase {
     Level& L = lv[l];
     Level& H = lv[l - 1];
     mark_begin(s, l, VK_DOWN);
-    if (fused_restrict_ok(L)) {
+    // width-2 patches: the group kernel fuses the restriction where the
+    // streaming kernel cannot (unsharded / replicated levels only)
+    if (fused_restrict_ok(L) || (group_w2(L) && !sharded(l))) {
       VisitDesc<T> v;
       v.src = SRC_LOAD;
       v.epi = true;

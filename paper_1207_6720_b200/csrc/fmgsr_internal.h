@@ -62,6 +62,8 @@ __host__ __device__ inline double pow4(int k) {
 enum { SHAPE_WIDE = 0, SHAPE_DEEP = 1, SHAPE_R4 = 2 };
 // SM sub-partitions (4 per SM) of the current device (kernels_visit.cu)
 int visit_smsps();
+// the short-patch group kernel (kernels_group.cu) is in use (FMGSR_VISIT_GROUP != 0)
+bool group_visit_enabled();
 inline bool is_pow2(i64 n) { return n >= 1 && (n & (n - 1)) == 0; }
 
 // Run f(); map exceptions to C return codes.

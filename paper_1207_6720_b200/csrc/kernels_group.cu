@@ -321,16 +321,6 @@ void launch_group_il(const GroupArgs<T>& a, size_t smem, cudaStream_t s) {
 #undef FMGSR_GROUP_IL
 }
 
-// FMGSR_VISIT_GROUP=0 keeps every visit on the streaming kernel (A/B runs)
-bool group_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FMGSR_VISIT_GROUP");
-    v = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return v == 1;
-}
-
 // widest owned width served here (FMGSR_GROUP_MAXW overrides, for A/B runs)
 int group_max_w() {
   static int v = -1;
@@ -344,13 +334,23 @@ int group_max_w() {
 
 }  // namespace
 
+// FMGSR_VISIT_GROUP=0 keeps every visit on the streaming kernel (A/B runs)
+bool group_visit_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FMGSR_VISIT_GROUP");
+    v = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // Short-patch visits (plain-load down visits with or without the fused
 // restriction, FAS-correction up visits; no Kaczmarz pass, uniform geometry).
 // Returns false when the visit is not of that kind: the caller then uses the
 // streaming kernel.
 template <typename T>
 bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s) {
-  if (!group_enabled() || d.olo || d.cr || d.fun_part || d.f64_arith) return false;
+  if (!group_visit_enabled() || d.olo || d.cr || d.fun_part || d.f64_arith) return false;
   if (!(d.src == SRC_LOAD || (d.src == SRC_CORR && !d.epi))) return false;
   // W = 16 measured slower than the streaming kernel (config 4 level 16: 49 / 42 us
   // against 40 / 33 us per down / up visit): two chains per group leave two of

@@ -157,12 +157,12 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
   if (d.src == SRC_FMG) require(d.uH && d.n >= 8, "visit: FMG needs uH with >= 4 coarse cells");
   if (d.cr && d.src != SRC_FMG) require(d.uc != nullptr, "visit: CR needs uc");
   if (d.epi) {
-    require(d.W >= 4 && d.n >= 8, "visit: fused restriction needs owned width >= 4");
     require(d.fH_out && d.E && d.cnt, "visit: epilogue buffers missing");
   } else {
     require(d.u_out != nullptr || d.fun_part != nullptr, "visit: u_out is null");
   }
-  if (try_group_visit(d, s)) return;
+  if (try_group_visit(d, s)) return;  // short patches (fuses the restriction from W = 2)
+  if (d.epi) require(d.W >= 4 && d.n >= 8, "visit: fused restriction needs owned width >= 4");
   if (d.f64_arith) {
     require(!d.fun_part, "visit: no functional output with fp64 arithmetic on fp32 fields");
     visit_launch_mixed(d, visit_cpl2_ok(d), visit_few_chains(d), s);

@@ -29,7 +29,11 @@ def _batch(n, B, seed):
     return torch.randn(n, B, generator=g, device="cuda", dtype=torch.float64)
 
 
-CASES = [(1024, 64, 16, 4), (1024, 33, 64, 1), (512, 128, 8, 3), (2048, 64, 2048, 0), (256, 1, 4, 8)]
+CASES = [(1024, 64, 16, 4), (1024, 33, 64, 1), (512, 128, 8, 3), (2048, 64, 2048, 0), (256, 1, 4, 8),
+         # short patches (owned width <= 8: the group kernel, kernels_group.cu): two and
+         # four interleaved chains per lane, odd / zero buffers, ragged column counts
+         (16384, 64, 4, 8), (16384, 96, 2, 8), (8192, 40, 8, 5), (4096, 33, 4, 1), (2048, 64, 8, 0),
+         (64, 5, 2, 8), (32, 70, 4, 3)]
 
 
 @pytest.mark.parametrize("n,B,W,b", CASES)
@@ -62,6 +66,8 @@ def test_visit_down_matches_composition(fm, oracle, n, B, W, b):
     f = _batch(n, B, 4) * 1e3
     for _ in range(2):  # the workspace counters return to their start state
         un, uH, fH = visits.visit_down(u, f, W, b)
+    un2, none_uH, fH2 = visits.visit_down(u, f, W, b, restrict_u=False)
+    assert none_uH is None and torch.equal(un2, un) and torch.equal(fH2, fH)
     uh, fh = u.cpu().numpy(), f.cpu().numpy()
     for r in range(B):
         ur = _smooth(oracle, uh[:, r], fh[:, r], n, W, b)
