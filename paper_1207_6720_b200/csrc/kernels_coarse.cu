@@ -16,12 +16,8 @@
 //
 // The same launch also hosts the multi-level restriction of the forcing
 // (the f cascade, cycles.py:178-180).
-#include <cooperative_groups.h>
-
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
-#include <string>
 #include <type_traits>
 
 #include "fmgsr_device.cuh"
@@ -29,8 +25,6 @@
 #include "fmgsr_internal.h"
 
 namespace fmgsr {
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -139,37 +133,6 @@ struct CoarseCtx {
     for (int e = threadIdx.x; e < n * CW; e += blockDim.x) {
       int i = e / CW, c = e % CW, col = c0 + c;
       if (col < a.B) dst[(i64)i * a.ld + col] = cvt<M>(src[e]);
-    }
-  }
-
-  // ---- column groups narrower than a 64-byte row segment (CW < 8) ---------------
-  // One CTA reading its own CW columns touches one 8- to 32-byte piece of every
-  // row: each element costs the SM a whole 32-byte sector request (config 4,
-  // CW = 1, level 12: 8192 requests per field, the load 19 k and the store 7.5 k
-  // of a V segment's 108 k cycles).  Launched as a thread-block cluster of
-  // G = 8 / CW CTAs (adjacent column groups), each CTA instead moves whole
-  // G CW-column row segments for 1/G of the rows and scatters / gathers the
-  // other CTAs' columns through distributed shared memory.  `dst` / `src` are
-  // the same shared-memory address in every CTA of the cluster.
-  __device__ void load_cluster(cg::cluster_group& cl, T* dst, const M* src, int n) {
-    const int G = (int)cl.num_blocks(), rk = (int)cl.block_rank();
-    const int cols = G * CW, cbase = c0 - rk * CW;  // the cluster's first column
-    const int rows = n / G, r0 = rk * rows;         // n is a power of two >= 8 >= G
-    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-      const int i = r0 + e / cols, c = e % cols, col = cbase + c;
-      const T v = col < a.B ? cvt<T>(src[(i64)i * a.ld + col]) : T(0);
-      T* peer = cl.map_shared_rank(dst, c / CW);
-      peer[i * CW + c % CW] = v;
-    }
-  }
-  __device__ void store_cluster(cg::cluster_group& cl, M* dst, const T* src, int n) {
-    const int G = (int)cl.num_blocks(), rk = (int)cl.block_rank();
-    const int cols = G * CW, cbase = c0 - rk * CW;
-    const int rows = n / G, r0 = rk * rows;
-    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
-      const int i = r0 + e / cols, c = e % cols, col = cbase + c;
-      const T* peer = cl.map_shared_rank(const_cast<T*>(src), c / CW);
-      if (col < a.B) dst[(i64)i * a.ld + col] = cvt<M>(peer[i * CW + c % CW]);
     }
   }
 
@@ -445,17 +408,10 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T, M> a
   x.rfac = e + n0;
   x.pjb = a.pj ? e + 2 * n0 : nullptr;
   x.fob = a.fo ? e + 2 * n0 + (a.pj ? (1 << Lc) * CW : 0) : nullptr;
-  cg::cluster_group cl = cg::this_cluster();
-  const bool clustered = cl.num_blocks() > 1;  // CW < 8: rows move as whole 64-byte segments
   if (a.mode == 0) {
     if (x.fob) {
       x.cascade_on_chip(Lc);
       x.copy(x.Fl(m0), x.FO(m0), n0);
-    } else if (clustered) {
-      // every level's forcing at once (each Fl(t) is written only here)
-      cl.sync();  // every CTA of the cluster is running: its shared memory may be written
-      for (int t = m0; t <= Lc; t++) x.load_cluster(cl, x.Fl(t), a.forig[t], 1 << t);
-      cl.sync();
     } else {
       x.load(x.Fl(m0), a.forig[m0], n0);
     }
@@ -463,7 +419,7 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T, M> a
     x.visit_direct();
     for (int t = m0 + 1; t <= Lc; t++) {
       if (x.fob) x.copy(x.Fl(t), x.FO(t), 1 << t);
-      else if (!clustered) x.load(x.Fl(t), a.forig[t], 1 << t);
+      else x.load(x.Fl(t), a.forig[t], 1 << t);
       x.bar("load", t);
       x.visit_top(t);
       for (int l = t - 1; l > m0; l--) x.visit_down(l);
@@ -471,27 +427,14 @@ __global__ void __launch_bounds__(CNT, 1) coarse_kernel(const CoarseArgs<T, M> a
       for (int l = m0 + 1; l <= t; l++) x.visit_up(l);
     }
   } else {
-    if (clustered) {
-      cl.sync();
-      x.load_cluster(cl, x.U(Lc, 0), a.u_top, 1 << Lc);
-      x.load_cluster(cl, x.Fl(Lc), a.f_top, 1 << Lc);
-      cl.sync();
-    } else {
-      x.load(x.U(Lc, 0), a.u_top, 1 << Lc);
-      x.load(x.Fl(Lc), a.f_top, 1 << Lc);
-    }
+    x.load(x.U(Lc, 0), a.u_top, 1 << Lc);
+    x.load(x.Fl(Lc), a.f_top, 1 << Lc);
     x.bar("load", Lc);
     for (int l = Lc; l > m0; l--) x.visit_down(l);
     x.visit_direct();
     for (int l = m0 + 1; l <= Lc; l++) x.visit_up(l);
   }
-  if (clustered) {
-    cl.sync();  // every CTA's result is complete
-    x.store_cluster(cl, a.u_top, x.U(Lc, x.cur(Lc)), 1 << Lc);
-    cl.sync();  // no CTA exits while a peer still reads its shared memory
-  } else {
-    x.store(a.u_top, x.U(Lc, x.cur(Lc)), 1 << Lc);
-  }
+  x.store(a.u_top, x.U(Lc, x.cur(Lc)), 1 << Lc);
   x.bar("store", Lc);
   x.dump();
 }
@@ -535,52 +478,11 @@ size_t coarse_smem_bytes(int m0, int Lc, int CW, int extra_cells) {
   return (size_t)(3 * cells * CW + 3 * ((i64)1 << m0) + (i64)extra_cells * CW) * sizeof(T);
 }
 
-// FMGSR_COARSE_CLUSTER=0 keeps the per-CTA column loads (A/B runs)
-static bool coarse_cluster_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FMGSR_COARSE_CLUSTER");
-    v = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <typename T, int CW, typename M>
 static void launch_coarse_cw(const CoarseArgs<T, M>& a, size_t smem, cudaStream_t s) {
   const int granted = smem_optin((const void*)coarse_kernel<T, CW, M>);
   require(smem <= (size_t)granted, "coarse: shared memory budget exceeded");
   unsigned blocks = (unsigned)((a.B + CW - 1) / CW);
-  // narrow column groups: clusters of G = 8 / CW CTAs move whole 64-byte row
-  // segments (load_cluster / store_cluster); the whole-solve mode with its
-  // on-chip cascade and the single-CTA launches stay as they are
-  constexpr int G = CW < 8 ? 8 / CW : 1;
-  if (G > 1 && blocks % G == 0 && !a.fo && coarse_cluster_enabled()) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(CNT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    // a cluster needs G SMs of one GPC free at this shared-memory size
-    static thread_local int ok_cache[2] = {-1, -1};  // per kernel instantiation and thread
-    int& okc = ok_cache[0];
-    if (okc < 0) {
-      int nclusters = 0;
-      cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, coarse_kernel<T, CW, M>, &cfg);
-      if (e != cudaSuccess) cudaGetLastError();
-      okc = (e == cudaSuccess && nclusters >= 1) ? 1 : 0;
-    }
-    if (okc == 1) {
-      check_cuda(cudaLaunchKernelEx(&cfg, coarse_kernel<T, CW, M>, a), "coarse cluster launch");
-      return;
-    }
-  }
   coarse_kernel<T, CW, M><<<blocks, CNT, smem, s>>>(a);
 }
 

@@ -1,26 +1,29 @@
 // kernels_group.cu -- level visits of SHORT patches (owned width W <= 8).
 //
-// On the mid levels of a deep hierarchy (config 4: levels 13-16, 4096 patches
-// of 2-16 cells with an 8-cell buffer) a patch chain is 10-24 cells long, so
+// On the mid levels of a deep hierarchy (config 4: levels 13-15, 4096 patches
+// of 2-8 cells with an 8-cell buffer) a patch chain is 10-16 cells long, so
 // the streaming visit_kernel is all head and tail: its ring staging, the
 // general boundary step and one fence + counter round per patch cost ~2000
 // instructions and ~18 k cycles per warp for ~1800 cycles of Gauss-Seidel
-// (ncu, profiles/r02/mid_levels_config4.txt).  Here one warp owns a GROUP of G
-// consecutive patches x 32 RHS columns instead:
+// (ncu, profiles/r02/mid_levels_config4.txt).  Here one CTA of four warps owns
+// a GROUP of G consecutive patches x 32 RHS columns (one lane per column):
 //   * the group's window (G W + b + 2 rows of u, f; the FAS-correction source
 //     rows on an up visit) is fetched once, every row in flight at the same
-//     time (cp.async into a per-lane column of shared memory, one wait);
+//     time (cp.async into per-lane columns of shared memory, one wait), the
+//     rows dealt round-robin to the warps;
 //   * on an up visit the smoother input u + P(uH - R u) (cycles.py:120-121,
 //     stencils.py:39-64) is built for the whole window in a data-parallel
 //     pass -- the expressions of PairSource<SRC_CORR>::make;
 //   * the G patch chains (additive smoother, _kernels_numba.py:60-92: every
-//     patch starts from the same input) are independent, so a lane runs IL of
-//     them interleaved -- the per-cell arithmetic and order of each chain are
-//     the reference's, only the schedule differs;
+//     patch starts from the same input) are independent, so they are dealt to
+//     the warps and a lane runs IL of them interleaved -- the per-cell
+//     arithmetic and order of each chain are the reference's, only the
+//     schedule differs;
 //   * restriction + tau (stencils.py:108-125) run over the group's smoothed
-//     cells with the Epilogue of the streaming kernel, and only the GROUP
-//     boundaries go through the edge-record protocol: one fence and counter
-//     round per G patches, and any owned width >= 2 fuses (G W >= 4).
+//     cells, a contiguous run of coarse cells per warp with the expressions of
+//     Epilogue::push / finish, and only the GROUP boundaries go through the
+//     edge-record protocol: one fence and counter round per G patches, and
+//     any owned width >= 2 fuses (G W >= 4).
 // Edge records, counters and the shard outbox keep the streaming kernel's
 // layout and indices (boundary = absolute patch index), so both kernels can
 // serve different visits of one level.
