@@ -220,7 +220,7 @@ struct Plan : PlanBase {
   // short-patch group kernel serves the down visits (a group owns >= 4 cells).
   bool group_w2(const Level& L) const {
     return d.fused && d.ns == 1 && !d.nonlinear && !mixed && L.W == 2 && L.n >= 8 &&
-           group_visit_enabled();
+           L.b <= 32 && group_visit_enabled();  // try_group_visit's own limits
   }
   bool epi_level(const Level& L) const { return L.W >= 4 || group_w2(L); }
 

@@ -66,6 +66,9 @@ def fm_global(sm):
     (12, 1024, 8, 1, 1),
     (12, 256, 4, 2, 1),
     (13, 4096, 8, 1, 1),     # config 4 geometry (W = 2 on every level)
+    (14, 4096, 8, 1, 1),     # ... with a width-4 finest level: group kernel on every grid level
+    (11, 512, 40, 1, 1),     # buffer beyond the group kernel's limit: width-2 levels unfused
+    (11, 256, 33, 0, 1),     # width 8 with a 33-cell buffer (streaming kernel), no SR
     (10, 16, 4, 1, 2),       # V(2,2)
     (10, 8, 3, 0, 2),
 ])
