@@ -767,7 +767,7 @@ struct Plan : PlanBase {
     mark_begin(s, t, VK_TOP);
     T* uH_in = H.u[H.cur];
     T* uH_out = H.u[H.cur ^ 1];
-    if (fused_restrict_ok(L)) {
+    if (fused_restrict_ok(L) || (group_w2(L) && !sharded(t))) {
       VisitDesc<T> v;
       v.src = SRC_FMG;
       v.epi = true;

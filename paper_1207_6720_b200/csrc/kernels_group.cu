@@ -107,6 +107,52 @@ __global__ void __launch_bounds__(GROUP_NT) group_visit_kernel(const GroupArgs<T
     cp_commit();
     cp_wait<0>();
     __syncthreads();
+  } else if (SRC == SRC_FMG) {
+    // Pi(uH) on the pairs [q0, q1] (stencils.py:67-105): coarse cells q-2 .. q+2,
+    // and the four cells next to a domain end for its special rows
+    const i64 nc = a.nc;
+    const i64 q0 = ulo >> 1, q1 = (uhi - 1) >> 1;
+    i64 h0 = q0 - 2 > 0 ? q0 - 2 : 0, h1 = q1 + 2 < nc - 1 ? q1 + 2 : nc - 1;
+    if (q0 <= 1 && h1 < 3) h1 = 3;            // rows 0-3 read c[0..3]
+    if (q1 >= nc - 2 && h0 > nc - 4) h0 = nc - 4;  // rows nf-4..nf-1 read c[nc-4..nc-1]
+    ubase = 2 * q0;
+    const int nh = (int)(h1 - h0 + 1);
+    {
+      const T* sh = a.uH + rr + (h0 + w) * ld;
+      for (int k = w; k < nh; k += NW, sh += NW * ld) cp_async(Hs + k * 32, sh);
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    auto C = [&](i64 j) { return Hs[(int)(j - h0) * 32]; };
+    for (i64 q = q0 + w; q <= q1; q += NW) {  // PairSource<SRC_FMG>::make, pair q
+      T e, o;
+      if (q >= 2 && q <= nc - 3) {
+        const T c0 = C(q - 2), c1 = C(q - 1), c2 = C(q), c3 = C(q + 1), c4 = C(q + 2);
+        e = xsub(xadd(xadd(xmul(T(-5), c0), xmul(T(35), c1)), xmul(T(105), c2)), xmul(T(7), c3));
+        o = xsub(xadd(xadd(xmul(T(-7), c1), xmul(T(105), c2)), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == 0) {  // rows 0, 1 over c[0..2]
+        const T c2 = C(0), c3 = C(1), c4 = C(2);
+        e = xsub(xmul(T(70), c2), xmul(T(2), c3));
+        o = xsub(xadd(xmul(T(112), c2), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == 1) {  // rows 2, 3 over c[0..3]
+        const T c1 = C(0), c2 = C(1), c3 = C(2), c4 = C(3);
+        e = xsub(xadd(xmul(T(40), c1), xmul(T(105), c2)), xmul(T(7), c3));
+        o = xsub(xadd(xadd(xmul(T(-7), c1), xmul(T(105), c2)), xmul(T(35), c3)), xmul(T(5), c4));
+      } else if (q == nc - 2) {  // rows nf-4, nf-3
+        const T c0 = C(nc - 4), c1 = C(nc - 3), c2 = C(nc - 2), c3 = C(nc - 1);
+        e = xsub(xadd(xadd(xmul(T(-7), c3), xmul(T(105), c2)), xmul(T(35), c1)), xmul(T(5), c0));
+        o = xsub(xadd(xmul(T(40), c3), xmul(T(105), c2)), xmul(T(7), c1));
+      } else {  // q == nc - 1: rows nf-2, nf-1
+        const T c0 = C(nc - 3), c1 = C(nc - 2), c2 = C(nc - 1);
+        e = xsub(xadd(xmul(T(112), c2), xmul(T(35), c1)), xmul(T(5), c0));
+        o = xsub(xmul(T(70), c2), xmul(T(2), c1));
+      }
+      const int k = (int)(q - q0);
+      Us[(2 * k) * 32] = xmul(e, T(0.0078125));  // x / 128 == x * 2^-7 exactly
+      Us[(2 * k + 1) * 32] = xmul(o, T(0.0078125));
+    }
+    __syncthreads();
   } else {
     // u + P(uH - R u) on the pairs [q0, q1] needs c = uH - R u one pair further out
     const i64 nc = a.nc;
@@ -347,14 +393,15 @@ bool group_visit_enabled() {
   return v == 1;
 }
 
-// Short-patch visits (plain-load down visits with or without the fused
-// restriction, FAS-correction up visits; no Kaczmarz pass, uniform geometry).
+// Short-patch visits (FMG-prolongation top visits and plain-load down visits,
+// each with or without the fused restriction, FAS-correction up visits; no
+// Kaczmarz pass, uniform geometry).
 // Returns false when the visit is not of that kind: the caller then uses the
 // streaming kernel.
 template <typename T>
 bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s) {
   if (!group_visit_enabled() || d.olo || d.cr || d.fun_part || d.f64_arith) return false;
-  if (!(d.src == SRC_LOAD || (d.src == SRC_CORR && !d.epi))) return false;
+  if (!(d.src == SRC_LOAD || d.src == SRC_FMG || (d.src == SRC_CORR && !d.epi))) return false;
   // W = 16 measured slower than the streaming kernel (config 4 level 16: 49 / 42 us
   // against 40 / 33 us per down / up visit): two chains per group leave two of
   // the four warps without chain work
@@ -386,7 +433,7 @@ bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s) {
   const int gw = G * a.W;
   a.rows_f = gw + a.b;
   a.rows_u = d.src == SRC_LOAD ? gw + a.b + 2 : gw + a.b + 10;
-  a.rows_h = d.src == SRC_LOAD ? 0 : a.rows_u / 2;
+  a.rows_h = d.src == SRC_LOAD ? 0 : a.rows_u / 2 + (d.src == SRC_FMG ? 8 : 0);
   a.gc = make_coef<T>(d.n, d.omega);
   a.inv_H2 = (T)pow4(level_of(d.n) - 1);
   a.write_u = d.write_u;
@@ -407,6 +454,9 @@ bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s) {
   if (d.src == SRC_LOAD) {
     if (d.epi) launch_group_il<T, SRC_LOAD, true>(a, smem, s);
     else launch_group_il<T, SRC_LOAD, false>(a, smem, s);
+  } else if (d.src == SRC_FMG) {
+    if (d.epi) launch_group_il<T, SRC_FMG, true>(a, smem, s);
+    else launch_group_il<T, SRC_FMG, false>(a, smem, s);
   } else {
     launch_group_il<T, SRC_CORR, false>(a, smem, s);
   }
