@@ -26,6 +26,8 @@ CASES = [  # m, P, b, n_sr, ns, nl, B, plan options
     (10, 8, 2, 1, 2, True, 32, dict()),                   # V(2,2) nonlinear
     (10, 16, 3, 0, 2, False, 32, dict()),                 # V(2,2) linear
     (10, 4, 2, 1, 1, False, 1, dict()),                   # whole solve on chip
+    (12, 1024, 8, 1, 1, False, 64, dict(coarse=0)),       # short patches: the group kernel on every level
+    (12, 512, 5, 2, 1, False, 40, dict(coarse=5)),        # ... odd buffer, ragged batch, two SR levels
 ]
 
 
