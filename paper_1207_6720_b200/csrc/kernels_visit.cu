@@ -63,6 +63,9 @@ static bool visit_few_chains(const VisitDesc<T>& d) {
 template <typename T>
 bool try_group_visit(const VisitDesc<T>& d, cudaStream_t s);
 
+// FAS-correction up visits with several patches per warp (kernels_visit_mp.cu)
+bool visit_up_mp(const VisitDesc<double>& d, bool r4, cudaStream_t s);
+
 // the fills live in kernels_visit_{d,f,v2d,v2f}.cu (one instantiation each,
 // compiled in parallel)
 template <typename TV, typename T, int SHAPE, typename TM = TV>
@@ -170,6 +173,11 @@ void launch_visit(const VisitDesc<T>& d, cudaStream_t s) {
     bool r4 = false;
     if constexpr (std::is_same<T, double>::value) {
       r4 = visit_r4(d);
+      // up visits of launches that overfill the warp slots: several patches per warp
+      if (visit_up_mp(d, r4, s)) {
+        check_launch("visit_up_mp_kernel");
+        return;
+      }
       if (r4) visit_fill_launch<V2<T>, T, SHAPE_R4>(d, s);
     }
     if (!r4) visit_fill_launch<V2<T>, T, SHAPE_WIDE>(d, s);
